@@ -1,0 +1,408 @@
+"""Benchmark: raked motion validation (BASELINE config 2) on B200, one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg3|cfg4|cfg5_<P>_<log2N>]
+
+Headline (default): BASELINE.json config 2 - 4,096 arm7 ("Panda" stand-in)
+edges, resolution 1/32, 24 cuboids + 8 capsules; one step = validate every
+edge (one kernel launch).  ``value`` = edges/s over all ranks with inputs
+resident in HBM; ``e2e`` = the same through the public API with the edges
+copied from pinned host memory and the verdict bits read back every step.
+The FK+CC batch workloads (configs 1, 3, 4) are reported alongside under
+``fkcc`` (configs/s and % of the FP32 roofline).
+
+Multi-GPU: one process per GPU (torchrun), every rank validates its own
+4,096-edge batch (weak scaling, no data-path collective - the path shards
+into independent edges); time = max over ranks.
+
+``--impl reference`` times the reference algorithm on the host CPU cores:
+the oracle port (oracle/vecmp_oracle.py, a bit-exact restatement of the
+pure-Python reference) with W = 8 blocks as the reference runs it, one
+process per core, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L2_FLUSH_BYTES = 256 << 20          # > 126 MB L2
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+SMS = 148
+FMA_PER_CLK = 128
+
+
+# ----------------------------------------------------------------- helpers
+
+def fp32_peak_tflops() -> tuple[float, str]:
+    mhz = 1965.0
+    src = "nominal sm_max_mhz 1965"
+    if PEAKS.exists():
+        mhz = float(json.loads(PEAKS.read_text()).get("sm_max_mhz", mhz))
+        src = "MEASURED_PEAKS.json sm_max_mhz"
+    return SMS * FMA_PER_CLK * 2 * mhz * 1e6 / 1e12, \
+        f"148 SM x 128 FFMA/clk x 2 flop x {mhz:.0f} MHz ({src}); no tensor cores"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled in the background."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._drain, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _drain(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[2:]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def rake_state_counts(n: np.ndarray, blocks: np.ndarray, valid: np.ndarray, width: int = 32):
+    """States the rake must fully evaluate: all n for valid edges; for invalid
+    edges the in-range states of the iterations before the failing one."""
+    s = np.ceil(n / width).astype(np.int64)
+    full = n.copy()
+    done = np.where(valid, blocks, blocks - 1)            # completed iterations
+    # in-range states of iterations 1..d: sum_k min(max(n - k s, 0), d)
+    k = np.arange(width)[None, :]
+    per = np.clip(n[:, None] - k * s[:, None], 0, None)
+    part = np.minimum(per, done[:, None]).sum(axis=1)
+    return np.where(valid, full, part)
+
+
+# ----------------------------------------------------------- our GPU arm
+
+def run_ours(args, rank: int, world: int) -> dict | None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2309_14545_b200 import ValidationContext, codegen, load_robot, workloads
+    from paper_2309_14545_b200 import motion as M
+    from paper_2309_14545_b200 import runtime
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    peak, peak_src = fp32_peak_tflops()
+
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    E = len(mw.starts)
+    sd = torch.from_numpy(mw.starts).cuda()
+    gd = torch.from_numpy(mw.goals).cuda()
+    bits = torch.empty((E + 31) // 32, dtype=torch.int32, device="cuda")
+    ws = torch.empty(1, dtype=torch.int32, device="cuda")
+    n_states = torch.empty(E, dtype=torch.int32, device="cuda")
+    blocks = torch.empty(E, dtype=torch.int32, device="cuda")
+    mod, denv = ctx.module, ctx.device_env
+    stream = torch.cuda.current_stream()
+
+    def step():
+        runtime.validate_motions_device(mod, denv, sd, gd, mw.resolution, width=32,
+                                        prune=True, bits=bits, workspace=ws)
+
+    # per-edge counts for the roofline numerator (one extra untimed launch)
+    b0, ns_t, bl_t = runtime.validate_motions_device(mod, denv, sd, gd, mw.resolution, width=32,
+                                                     prune=True, want_counts=True)
+    valid = runtime.unpack_bits(b0.cpu().numpy(), E)
+    n_np, b_np = ns_t.cpu().numpy().astype(np.int64), bl_t.cpu().numpy().astype(np.int64)
+    states = rake_state_counts(n_np, b_np, valid)
+    f_cfg = codegen.algorithmic_flops(rob.program, rob.pairs, denv.counts)["total"]
+    f_state = f_cfg + 3 * rob.tree.dof                    # + interpolation
+    flops_per_launch = float(states.sum()) * f_state
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        for a, b in ev:
+            flush.zero_()                                 # L2 flush between timed steps
+            a.record(stream)
+            step()
+            b.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kernel_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(kernel_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * E / (ms_per_step / 1e3)
+    avg_launch_ms = float(np.mean(kernel_ms))
+    achieved = flops_per_launch / (avg_launch_ms / 1e3) / 1e12
+
+    # ---- end to end through the public API, host buffers
+    hs = torch.from_numpy(mw.starts).pin_memory()
+    hg = torch.from_numpy(mw.goals).pin_memory()
+    hb = torch.empty(bits.shape, dtype=torch.int32).pin_memory()
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    sd2 = torch.empty_like(sd)
+    gd2 = torch.empty_like(gd)
+    for i in range(args.warmup + args.steps):
+        if i >= args.warmup:
+            flush.zero_()
+            a, b = e2e_ev[i - args.warmup]
+            a.record(stream)
+        sd2.copy_(hs, non_blocking=True)
+        gd2.copy_(hg, non_blocking=True)
+        out = M.validate_motions(ctx, sd2, gd2, mw.resolution, bits=bits, workspace=ws)
+        hb.copy_(out, non_blocking=True)
+        if i >= args.warmup:
+            b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = float(sum(a.elapsed_time(b) for a, b in e2e_ev))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * E / (e2e_ms / args.steps / 1e3)
+    assert runtime.unpack_bits(hb.numpy(), E).tolist() == valid.tolist()
+
+    fkcc = {} if args.no_aux else fkcc_summary(ctx_flush=flush, peak=peak)
+    if rank != 0:
+        return None
+    line = {
+        "metric": "validated edges/sec (raked motion validation, BASELINE config 2)",
+        "value": round(value, 1),
+        "unit": "edges/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded; arm7 stand-in for Panda, see DESIGN.md)",
+        "config": {"workload": mw.name, "robot": "arm7 (Panda stand-in)", "edges_per_gpu": E,
+                   "resolution": mw.resolution, "rake_width": 32,
+                   "obstacles": "24 cuboids + 8 capsules",
+                   "valid_edge_fraction": round(float(valid.mean()), 4),
+                   "mean_states_per_edge": round(float(n_np.mean()), 2),
+                   "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
+                   "parallelism": f"dp{world} (independent edges per rank)"},
+        "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "vmp_motion_p1_s2_g1",
+                     "algorithmic_flop_per_state": f_state,
+                     "states_counted_per_launch": int(states.sum()),
+                     "note": "states fully evaluated by the rake (valid edges: all n; invalid: "
+                             "iterations before the failing one) x reference dense flop/state; "
+                             "peak: " + peak_src},
+        "gpu_launches": args.steps,
+        "e2e": {"value": round(e2e_value, 1), "unit": "edges/s",
+                "h2d_bytes_per_step": int(mw.starts.nbytes + mw.goals.nbytes),
+                "d2h_bytes_per_step": int(bits.numel() * 4)},
+        "clocks": clocks.summary(),
+    }
+    if fkcc:
+        line["fkcc"] = fkcc
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline_motion(mw, rob, processes=1, n_edges=args.cpu_edges)
+    return line
+
+
+def fkcc_summary(ctx_flush, peak: float) -> dict:
+    """Configs 1/3/4 batch FK+CC: configs/s and % FP32 roofline (dense + early exit)."""
+    import torch
+
+    from paper_2309_14545_b200 import ValidationContext, codegen, load_robot, workloads
+    from paper_2309_14545_b200 import runtime
+
+    out = {}
+    for key, make in (("cfg1", workloads.config1), ("cfg3", workloads.config3),
+                      ("cfg4", workloads.config4)):
+        wl = make()
+        rob = load_robot(wl.robot)
+        ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+        qd = torch.from_numpy(wl.q).cuda()
+        n = qd.shape[1]
+        words = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        f = codegen.algorithmic_flops(rob.program, rob.pairs, ctx.device_env.counts)["total"]
+        res = {"robot": wl.robot, "configs": n, "flop_per_config": f}
+        for mode, early in (("early_exit", True), ("dense", False)):
+            for _ in range(3):
+                ctx.validate_batch(qd, early_exit=early, out=words)
+            times = []
+            for _ in range(10):
+                ctx_flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                ctx.validate_batch(qd, early_exit=early, out=words)
+                b.record()
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b))
+            ms = float(np.median(times))
+            rate = n / (ms / 1e3)
+            res[mode] = {"ms": round(ms, 4), "configs_per_s": round(rate, 1),
+                         "tflops": round(rate * f / 1e12, 3),
+                         "frac_fp32": round(rate * f / 1e12 / peak, 4)}
+        res["collision_rate"] = round(1 - float(runtime.unpack_bits(words.cpu().numpy(), n).mean()), 4)
+        out[key] = res
+    return out
+
+
+# ------------------------------------------------------- CPU reference arm
+
+def _cpu_worker(payload):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import vecmp_oracle as O
+    from paper_2309_14545_b200 import load_robot, workloads
+    idx = payload
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    ob = O.Obstacles(mw.env.primitives)
+    t0 = time.perf_counter()
+    verdicts = [O.rake_check(rob.program, rob.pairs, ob, mw.starts[i], mw.goals[i], mw.resolution, 8)[0]
+                for i in idx]
+    return time.perf_counter() - t0, verdicts
+
+
+def cpu_baseline_motion(mw, rob, processes: int, n_edges: int) -> dict:
+    """Oracle port (bit-exact restatement of the reference) on host cores:
+    ValidationContext(width=8)-style rake per edge, as the reference runs it."""
+    rng = np.random.default_rng(123)
+    idx = np.sort(rng.choice(len(mw.starts), size=min(n_edges, len(mw.starts)), replace=False))
+    chunks = [idx[i::processes] for i in range(processes)]
+    t0 = time.perf_counter()
+    if processes == 1:
+        results = [_cpu_worker(chunks[0])]
+    else:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(processes) as pool:
+            results = pool.map(_cpu_worker, chunks)
+    wall = time.perf_counter() - t0
+    return {"value": round(len(idx) / wall, 2), "unit": "edges/s", "cores": processes,
+            "kind": "port",
+            "sample": f"{len(idx)} seeded-random edges of the 4,096 (W=8 rake, numpy "
+                      f"{np.__version__}, {processes} process(es), {wall:.1f} s wall)"}
+
+
+def run_reference(args, rank: int, world: int) -> dict | None:
+    if rank != 0:
+        return None
+    from paper_2309_14545_b200 import load_robot, workloads
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    per_step = max(cores * 4, 64)
+    for _ in range(min(args.warmup, 1)):
+        cpu_baseline_motion(mw, rob, cores, min(per_step, 64))
+    vals = []
+    t_total = 0.0
+    for k in range(args.steps):
+        r = cpu_baseline_motion(mw, rob, cores, per_step)
+        vals.append(r["value"])
+        t_total += per_step / r["value"]
+    value = args.steps * per_step / t_total
+    return {
+        "impl": "reference",
+        "metric": "validated edges/sec (raked motion validation, BASELINE config 2)",
+        "value": round(value, 2), "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t_total / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded; arm7 stand-in for Panda)",
+        "config": {"workload": mw.name, "robot": "arm7 (Panda stand-in)", "resolution": mw.resolution,
+                   "edges_per_step": per_step},
+        "cpu_baseline": {"value": round(value, 2), "unit": "edges/s", "cores": cores, "kind": "port",
+                         "sample": f"{per_step} seeded-random edges per step, W=8 rake, one "
+                                   f"process per core"},
+        "e2e": {"value": round(value, 2), "unit": "edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+# -------------------------------------------------------------------- main
+
+def main() -> None:
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    p.add_argument("--no-aux", action="store_true", help="skip the FK+CC batch summary")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-edges", type=int, default=1024)
+    args = p.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    line = run_ours(args, rank, world) if args.impl == "ours" else run_reference(args, rank, world)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,134 @@
+/* vmp.h - C ABI of the B200 FK + collision-checking + motion-validation path.
+ *
+ * The reference (arxiv 2309.14545 package `vecmp`, pure Python/NumPy) has no
+ * FFI: its boundary is the Python API in pkg/src/vecmp/__init__.py:5-29.  This
+ * header is what a binding behind those Python names calls (our own shims in
+ * paper_2309_14545_b200/ use ctypes; INTEGRATION.md shows the binding a vecmp
+ * maintainer would add).  Each entry point cites the reference interface it
+ * replaces.  No C++ or torch types cross this boundary: plain pointers, sizes
+ * and an opaque CUDA stream handle (cudaStream_t / CUstream, NULL = legacy).
+ *
+ * Conventions
+ *   - return 0 on success, a negative VMP_E* code on failure; the thread-local
+ *     message is available from vmp_last_error().  VMP_EARG maps to Python
+ *     ValueError with the same text, VMP_ECUDA / VMP_ECOMPILE to RuntimeError.
+ *   - all batch buffers are caller-owned DEVICE memory; calls are asynchronous
+ *     on `stream`, perform no allocation, and handles are immutable after
+ *     creation, so concurrent calls on distinct streams are safe.
+ */
+#ifndef VMP_H
+#define VMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VMP_OK 0
+#define VMP_EARG (-1)     /* invalid argument            -> ValueError   */
+#define VMP_ECUDA (-2)    /* CUDA runtime / launch error -> RuntimeError */
+#define VMP_ECOMPILE (-3) /* NVRTC compile or load error -> RuntimeError */
+#define VMP_ENOMEM (-4)
+
+/* vmp_validate flags (reference collision.py:411-430 keyword arguments) */
+#define VMP_PRUNE 1u         /* coarse per-link sphere prune (prune=True)            */
+#define VMP_NO_EARLY_EXIT 4u /* dense mode: never stop a warp early (roofline runs)  */
+/* vmp_validate_motions flags (reference motion.py:38-90) */
+#define VMP_BACKWARD 16u     /* comb each stratum top-down (backward=True)            */
+
+typedef struct vmp_robot vmp_robot; /* compiled module for one KinematicProgram (+pairs) */
+typedef struct vmp_env vmp_env;     /* device-resident packed obstacles                   */
+
+typedef struct {
+  int32_t dof;       /* KinematicProgram.dof           (reference program.py:40-50) */
+  int32_t n_ops;     /* len(KinematicProgram)                                     */
+  int32_t n_markers; /* len(KinematicProgram.checks)                              */
+  int32_t has_cc;    /* module contains collision + motion kernels (pairs given)  */
+} vmp_robot_desc;
+
+/* Library version (major * 10000 + minor * 100 + patch). */
+int vmp_version(void);
+
+/* Thread-local text of the last error ("" if none). */
+const char *vmp_last_error(void);
+
+/* Compile CUDA source produced by codegen.py (the lowering of
+ * schedule_program's KinematicProgram, reference program.py:82-139) with
+ * NVRTC for sm_100a and write the cubin to `cubin_path`.  Needs no GPU. */
+int vmp_compile(const char *cuda_source, const char *name, const char *cubin_path);
+
+/* Load a cubin written by vmp_compile on the current device.  Replaces the
+ * reference's per-program interpreter state (program.py:56-74 dispatch_ops,
+ * Scratch program.py:142-154). */
+int vmp_robot_load(const char *cubin_path, const vmp_robot_desc *desc, vmp_robot **out);
+void vmp_robot_destroy(vmp_robot *robot);
+
+/* Pack obstacles into device records (reference collision.py:57-119
+ * _PackedEnvironment / Environment.packed(); cylinders arrive as capsules,
+ * collision.py:147-153).  Inputs are host float64, row-major:
+ *   spheres  n_spheres  x 4 : cx cy cz r
+ *   capsules n_capsules x 7 : p0(3) p1(3) r
+ *   boxes    n_boxes    x 15: centre(3) half_extents(3) rotation(9, row-major, world-from-box)
+ */
+int vmp_env_create(const double *spheres, int32_t n_spheres, const double *capsules,
+                   int32_t n_capsules, const double *boxes, int32_t n_boxes, vmp_env **out);
+void vmp_env_destroy(vmp_env *env);
+/* Bytes of the packed device records (shared-memory staging size). */
+int64_t vmp_env_bytes(const vmp_env *env);
+
+/* Every op row of the program for n configurations q (dof x ld, float32):
+ * rows (n_ops x ldo).  Replaces evaluate_program's lane loop
+ * (reference program.py:157-214) - the sink replay happens in the caller. */
+int vmp_fk_rows(const vmp_robot *robot, const float *q, int64_t n, int64_t ld, float *rows,
+                int64_t ldo, void *stream);
+
+/* Sphere centres only: rows 3m+{0,1,2} for marker m (n_markers*3 x ldo). */
+int vmp_fk_spheres(const vmp_robot *robot, const float *q, int64_t n, int64_t ld,
+                   float *centres, int64_t ldo, void *stream);
+
+/* Fused FK + self-collision + environment check of n configurations.
+ * valid_bits: ceil(n/32) words, bit (i % 32) of word i/32 set = VALID.
+ * Replaces validate_block / ValidationContext.validate_block
+ * (reference collision.py:411-430, 433-459) for any block width. */
+int vmp_validate(const vmp_robot *robot, const vmp_env *env, const float *q, int64_t n,
+                 int64_t ld, uint32_t flags, uint32_t *valid_bits, void *stream);
+
+/* Raked motion validation of n_edges straight-line motions (starts/goals:
+ * n_edges x sld float32, row-major).  Replaces raked_motion_check /
+ * validate_motion_rake (reference motion.py:38-90) batched over edges.
+ *   width      : rake width W whose block counts are reproduced (ctx.width);
+ *                32 is the native warp width
+ *   valid_bits : ceil(n_edges/32) words (zeroed by this call)
+ *   n_states   : optional, discretization_count per edge (motion.py:25-29)
+ *   blocks     : optional, block evaluations the W-wide rake performs
+ *   workspace  : >= 4 bytes of device scratch (persistent work queue) */
+int vmp_validate_motions(const vmp_robot *robot, const vmp_env *env, const float *starts,
+                         const float *goals, int64_t n_edges, int64_t sld, double resolution,
+                         int32_t width, uint32_t flags, uint32_t *valid_bits, int32_t *n_states,
+                         int32_t *blocks, void *workspace, void *stream);
+
+/* n = max(1, ceil(||g - s|| / resolution)) per edge with numpy float32
+ * reduction order (reference motion.py:25-29, lanes.py:106-113). */
+int vmp_discretize(const float *starts, const float *goals, int64_t n_edges, int32_t dim,
+                   int64_t sld, double resolution, int32_t *n_out, void *stream);
+
+/* Per-obstacle, per-lane contact of spheres of one radius against env
+ * (hits: n_obstacles x n bytes, 1 = contact, obstacle order spheres,
+ * capsules, boxes).  Backs sphere_vs_{sphere,capsule,cuboid}_lanes
+ * (reference collision.py:263-287) and BlockValidator. */
+int vmp_sphere_hits(const vmp_env *env, const float *xyz, int64_t n, int64_t ld, float radius,
+                    uint8_t *hits, void *stream);
+
+/* Select the CUDA device used by subsequent vmp calls on this thread (robots
+ * and environments remember the device they were created on). */
+int vmp_set_device(int32_t device);
+
+/* SM count of the current device and its ordinal (diagnostics). */
+int vmp_device_info(int32_t *sm_count, int32_t *device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,467 @@
+"""Lower a ``KinematicProgram`` (+ self-collision pairs) to sm_100a CUDA C++.
+
+This is the B200 counterpart of the reference's lane interpreter
+(pkg/src/vecmp/program.py:157-214 driving collision.py:293-408): instead of
+dispatching one numpy ufunc per op over W lanes, the op list becomes
+straight-line register code with one configuration per thread, compiled once
+per robot by NVRTC (csrc/vmp.cu) and cached as a cubin.
+
+Generated kernels (all take one by-value argument struct from csrc/vmp_abi.h):
+
+  vmp_fk_rows            every op row (evaluate_program's Scratch)
+  vmp_fk_spheres         3 rows per marker (sphere centres; HBM-bound kernel)
+  vmp_validate_p{P}_s{S} fused FK + self-collision + environment narrowphase,
+                         packed uint32 verdict bitmask (P: coarse prune,
+                         S: 0 dense, 1 stop when every lane of the warp is
+                         invalid = reference collision.py:403)
+  vmp_motion_p{P}_s{S}   warp-per-edge raked motion validation; S=2 stops at
+                         the first invalid lane (W multiple of 32), S=1 keeps
+                         exact W-block counts for any W
+
+Kernel structure: FK for all spheres first (cheap, ~150
+flop), then self pairs with compile-time thresholds, then an obstacle-major
+sweep - each obstacle record is read once from shared memory and tested
+against every config-dependent fine sphere held in registers.  Spheres whose
+centres are program constants (e.g. the arm7 base) are tested against the
+environment once per CTA, not once per configuration.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
+
+CSRC = Path(__file__).resolve().parent / "csrc"
+BLOCK = 128
+CODEGEN_VERSION = 3
+
+
+def f32_literal(value: float) -> str:
+    """Exact float32 literal (hex float) of ``np.float32(value)``."""
+    v = np.float32(value)
+    if v == 0:
+        return "-0.0f" if np.signbit(v) else "0.0f"
+    if not np.isfinite(v):
+        raise ValueError(f"non-finite constant {value!r} in program")
+    return f"{float(v).hex()}f".replace("0x", "0x")
+
+
+@dataclass(frozen=True)
+class FineSphere:
+    slot: int          # index among fine markers (program order)
+    link: int
+    index: int
+    radius: float
+    xyz: tuple         # op ids
+    const: bool        # centre independent of the configuration
+
+
+@dataclass(frozen=True)
+class RobotLayout:
+    """Everything codegen derives from (program, pairs)."""
+
+    dof: int
+    n_ops: int
+    n_markers: int
+    fine: tuple
+    coarse: dict       # link -> (radius, xyz) for links with >= 2 fine spheres
+    pairs: tuple       # (slot_a, slot_b, thr_f32)
+    has_cc: bool       # pairs given -> collision kernels emitted
+
+    @property
+    def dynamic(self) -> list:
+        return [s for s in self.fine if not s.const]
+
+    @property
+    def const_spheres(self) -> list:
+        return [s for s in self.fine if s.const]
+
+
+def derive_layout(program, pairs=None) -> RobotLayout:
+    kinds = np.asarray(program.kinds)
+    fine: list[FineSphere] = []
+    coarse_of: dict[int, tuple] = {}
+    per_link: dict[int, list[int]] = {}
+    for m in program.checks:
+        xyz = tuple(int(v) for v in m.xyz)
+        if m.level == FINE:
+            slot = len(fine)
+            const = all(int(kinds[v]) == CONST for v in xyz)
+            fine.append(FineSphere(slot, int(m.link), int(m.index), float(m.radius), xyz, const))
+            per_link.setdefault(int(m.link), []).append(slot)
+        else:
+            coarse_of[int(m.link)] = (float(m.radius), xyz)
+    coarse = {link: coarse_of[link] for link, slots in per_link.items()
+              if len(slots) >= 2 and link in coarse_of}
+    pair_list = []
+    if pairs is not None:
+        for lo, hi in sorted(tuple(sorted(p)) for p in pairs.pairs):
+            for sb in per_link.get(hi, ()):
+                for sa in per_link.get(lo, ()):
+                    ra, rb = fine[sa].radius, fine[sb].radius
+                    thr = np.float32(np.float32(rb + ra) * np.float32(rb + ra))
+                    pair_list.append((sa, sb, float(thr)))
+    return RobotLayout(dof=int(program.dof), n_ops=len(kinds), n_markers=len(program.checks),
+                       fine=tuple(fine), coarse=coarse, pairs=tuple(pair_list),
+                       has_cc=pairs is not None)
+
+
+def _fk_lines(program) -> list[str]:
+    """Straight-line float32 FK: one SSA value per op (contraction allowed)."""
+    kinds = [int(k) for k in program.kinds]
+    a = [int(x) for x in program.a]
+    b = [int(x) for x in program.b]
+    values = [float(x) for x in program.values]
+    cos_of = {a[i]: i for i, k in enumerate(kinds) if k == COS}
+    sin_of = {a[i]: i for i, k in enumerate(kinds) if k == SIN}
+    done: set[int] = set()
+    lines: list[str] = []
+    for i, k in enumerate(kinds):
+        if i in done:
+            continue
+        if k == CONST:
+            lines.append(f"const float v{i} = {f32_literal(values[i])};")
+        elif k == INPUT:
+            lines.append(f"const float v{i} = q[{int(values[i])}];")
+        elif k == ADD:
+            lines.append(f"const float v{i} = v{a[i]} + v{b[i]};")
+        elif k == SUB:
+            lines.append(f"const float v{i} = v{a[i]} - v{b[i]};")
+        elif k == MUL:
+            lines.append(f"const float v{i} = v{a[i]} * v{b[i]};")
+        elif k == NEG:
+            lines.append(f"const float v{i} = -v{a[i]};")
+        elif k in (SIN, COS):
+            arg = a[i]
+            si, ci = sin_of.get(arg), cos_of.get(arg)
+            if si is not None and ci is not None:
+                lines.append(f"float v{si}, v{ci}; sincosf(v{arg}, &v{si}, &v{ci});")
+                done.update((si, ci))
+            elif k == SIN:
+                lines.append(f"const float v{i} = sinf(v{arg});")
+            else:
+                lines.append(f"const float v{i} = cosf(v{arg});")
+        else:
+            raise ValueError(f"unknown op kind {k} at {i}")
+    return lines
+
+
+def _xyz(s: FineSphere) -> tuple[str, str, str]:
+    return tuple(f"v{v}" for v in s.xyz)
+
+
+def _state_function(lay: RobotLayout) -> str:
+    dyn = lay.dynamic
+    out = []
+    emit = out.append
+    emit("template <int STOP, bool PRUNE>")
+    emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
+    emit("                                          int ns, int nc, int nb, bool ok) {")
+    emit("  (void)env; (void)ns; (void)nc; (void)nb;")
+    for line in _FK_BODY_PLACEHOLDER:
+        emit(line)
+    emit("#define VMP_STOP_NOW ((STOP == 1 && !__any_sync(VMP_FULL, ok)) || "
+         "(STOP == 2 && __any_sync(VMP_FULL, !ok && vmp_inr)))")
+    emit("  const bool vmp_inr = ok;")
+    emit("  (void)vmp_inr;")
+    # self-collision pairs (compile-time thresholds)
+    fine = lay.fine
+    for sa, sb, thr in lay.pairs:
+        ax, ay, az = _xyz(fine[sa])
+        bx, by, bz = _xyz(fine[sb])
+        emit(f"  ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
+    emit("  if (VMP_STOP_NOW) return ok;")
+    # per-sphere constants
+    for s in dyn:
+        x, y, z = _xyz(s)
+        rs2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
+        emit(f"  const float S{s.slot} = vmp_sphere_S({x}, {y}, {z}, {f32_literal(rs2)});")
+    coarse_links = {link for link in lay.coarse}
+    by_link: dict[int, list[FineSphere]] = {}
+    for s in dyn:
+        by_link.setdefault(s.link, []).append(s)
+
+    def group_tests(test_fn, coarse_fn) -> None:
+        emitted_links = []
+        for link, spheres in by_link.items():
+            tests = [test_fn(s) for s in spheres]
+            if link in coarse_links and len(spheres) >= 2:
+                emit("    if (!PRUNE || __any_sync(VMP_FULL, !" + coarse_fn(link) + ")) {")
+                for t in tests:
+                    emit("      ok &= " + t + ";")
+                emit("    }")
+            else:
+                for t in tests:
+                    emit("    ok &= " + t + ";")
+            emitted_links.append(link)
+
+    def coarse_xyz(link):
+        r, xyz = lay.coarse[link]
+        return r, tuple(f"v{v}" for v in xyz)
+
+    def sph_test(s):
+        x, y, z = _xyz(s)
+        return f"vmp_clear_sphere({x}, {y}, {z}, S{s.slot}, {f32_literal(-2.0 * np.float32(s.radius))}, r0, r1.x)"
+
+    def sph_coarse(link):
+        r, (x, y, z) = coarse_xyz(link)
+        rs2 = np.float32(np.float32(r) * np.float32(r))
+        return (f"vmp_clear_sphere({x}, {y}, {z}, vmp_sphere_S({x}, {y}, {z}, {f32_literal(rs2)}), "
+                f"{f32_literal(-2.0 * np.float32(r))}, r0, r1.x)")
+
+    def cap_test(s):
+        x, y, z = _xyz(s)
+        return f"vmp_clear_capsule({x}, {y}, {z}, S{s.slot}, {f32_literal(-2.0 * np.float32(s.radius))}, r0, r1, r2)"
+
+    def cap_coarse(link):
+        r, (x, y, z) = coarse_xyz(link)
+        rs2 = np.float32(np.float32(r) * np.float32(r))
+        return (f"vmp_clear_capsule({x}, {y}, {z}, vmp_sphere_S({x}, {y}, {z}, {f32_literal(rs2)}), "
+                f"{f32_literal(-2.0 * np.float32(r))}, r0, r1, r2)")
+
+    def box_fn(radius):
+        return "vmp_clear_box_small" if radius < 1.0 else "vmp_clear_box_any"
+
+    def box_test(s):
+        x, y, z = _xyz(s)
+        rs2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
+        return f"{box_fn(s.radius)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
+
+    def box_coarse(link):
+        r, (x, y, z) = coarse_xyz(link)
+        rs2 = np.float32(np.float32(r) * np.float32(r))
+        return f"{box_fn(r)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
+
+    if dyn:
+        emit("  const float4 *p = env;")
+        emit("  for (int k = 0; k < ns; ++k, p += 2) {")
+        emit("    const float4 r0 = p[0], r1 = p[1];")
+        group_tests(sph_test, sph_coarse)
+        emit("    if (VMP_STOP_NOW) return ok;")
+        emit("  }")
+        emit("  for (int k = 0; k < nc; ++k, p += 3) {")
+        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2];")
+        group_tests(cap_test, cap_coarse)
+        emit("    if (VMP_STOP_NOW) return ok;")
+        emit("  }")
+        emit("  for (int k = 0; k < nb; ++k, p += 4) {")
+        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3];")
+        group_tests(box_test, box_coarse)
+        emit("    if (VMP_STOP_NOW) return ok;")
+        emit("  }")
+    emit("#undef VMP_STOP_NOW")
+    emit("  return ok;")
+    emit("}")
+    return "\n".join(out)
+
+
+_FK_BODY_PLACEHOLDER = ["  VMP_FK_BODY"]
+
+
+def _const_check(lay: RobotLayout) -> str:
+    """Per-CTA test of configuration-independent spheres against the env."""
+    consts = lay.const_spheres
+    lines = ["__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb) {",
+             "  (void)env; (void)ns; (void)nc; (void)nb;",
+             "  bool ok = true;"]
+    if consts:
+        lines.append("  switch (threadIdx.x) {")
+        for k, s in enumerate(consts):
+            # centre coordinates of a const sphere are CONST ops: exact float32 literals
+            lines.append(f"  case {k}: ok = vmp_sphere_clear_env(env, ns, nc, nb, "
+                         f"VMP_C{s.slot}X, VMP_C{s.slot}Y, VMP_C{s.slot}Z, {f32_literal(s.radius)}); break;")
+        lines.append("  default: break;")
+        lines.append("  }")
+    lines.append("  return ok;")
+    lines.append("}")
+    return "\n".join(lines)
+
+
+def _kernels(lay: RobotLayout, program) -> str:
+    dofp = max(1, lay.dof)
+    ld_q = "\n".join(f"    q[{j}] = __ldg(a.q + {j} * a.ld + ii);" for j in range(lay.dof))
+    rows = "\n".join(f"    o[{i} * a.ldo] = v{i};" for i in range(lay.n_ops))
+    centre_rows = []
+    for m, marker in enumerate(program.checks):
+        for c, v in enumerate(marker.xyz):
+            centre_rows.append(f"    o[{3 * m + c} * a.ldo] = v{int(v)};")
+    centre_rows = "\n".join(centre_rows)
+    src = f"""
+extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_rows(VmpFkArgs a) {{
+  for (long long i = blockIdx.x * (long long){BLOCK} + threadIdx.x; i < a.n;
+       i += (long long)gridDim.x * {BLOCK}) {{
+    const long long ii = i;
+    float q[{dofp}];
+{ld_q}
+    VMP_FK_BODY
+    float *o = a.out + i;
+{rows}
+  }}
+}}
+
+extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_spheres(VmpFkArgs a) {{
+  for (long long i = blockIdx.x * (long long){BLOCK} + threadIdx.x; i < a.n;
+       i += (long long)gridDim.x * {BLOCK}) {{
+    const long long ii = i;
+    float q[{dofp}];
+{ld_q}
+    VMP_FK_BODY
+    float *o = a.out + i;
+{centre_rows}
+  }}
+}}
+"""
+    if not lay.has_cc:
+        return src
+    src += f"""
+template <int PRUNE, int STOP, bool STAGED>
+__device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
+  extern __shared__ float4 vmp_smem[];
+  __shared__ unsigned long long vmp_bar;
+  const float4 *env = a.env.rec;
+  if (STAGED) {{
+    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
+    __syncthreads();
+    vmp_mbar_wait(&vmp_bar, 0);
+    env = vmp_smem;
+  }}
+  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+  const long long stride = (long long)gridDim.x * {BLOCK};
+  for (long long base = blockIdx.x * (long long){BLOCK}; base < a.n; base += stride) {{
+    const long long i = base + threadIdx.x;
+    const bool inr = i < a.n;
+    const long long ii = inr ? i : a.n - 1;
+    float q[{dofp}];
+{ld_q}
+    const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
+    const unsigned m = __ballot_sync(VMP_FULL, ok);
+    if ((threadIdx.x & 31) == 0 && inr) a.bits[i >> 5] = m;
+  }}
+}}
+
+template <int PRUNE, int STOP, bool STAGED>
+__device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
+  extern __shared__ float4 vmp_smem[];
+  __shared__ unsigned long long vmp_bar;
+  const float4 *env = a.env.rec;
+  if (STAGED) {{
+    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
+    __syncthreads();
+    vmp_mbar_wait(&vmp_bar, 0);
+    env = vmp_smem;
+  }}
+  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+  const int lane = threadIdx.x & 31;
+  const long long W = a.width;
+  for (;;) {{
+    unsigned e = 0;
+    if (lane == 0) e = atomicAdd(a.queue, 1u);
+    e = __shfl_sync(VMP_FULL, e, 0);
+    if ((long long)e >= a.n_edges) break;
+    float s[{dofp}], g[{dofp}];
+#pragma unroll
+    for (int j = 0; j < {lay.dof}; ++j) {{
+      s[j] = __ldg(a.starts + (long long)e * a.sld + j);
+      g[j] = __ldg(a.goals + (long long)e * a.sld + j);
+    }}
+    const long long n = vmp_discretize<{lay.dof}>(s, g, a.resolution);
+    const long long S = (n + W - 1) / W;
+    const long long total = S * W;
+    bool verdict = true;
+    long long blocks = S;
+    if (!cclear) {{
+      verdict = false;
+      blocks = 1;
+    }} else {{
+      for (long long base = 0; base < total; base += 32) {{
+        const long long p = base + lane;
+        const long long j = p / W + 1;
+        const long long k = p - (j - 1) * W;
+        const long long idx = k * S + (a.backward ? (S - j + 1) : j);
+        const bool inr = p < total && idx <= n;
+        const float t = vmp_rake_param(inr ? idx : 1, n);
+        float q[{dofp}];
+#pragma unroll
+        for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], t);
+        const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr);
+        const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
+        if (bad) {{
+          verdict = false;
+          blocks = (base + __ffs(bad) - 1) / W + 1;
+          break;
+        }}
+      }}
+    }}
+    if (lane == 0) {{
+      if (verdict) atomicOr(a.bits + (e >> 5), 1u << (e & 31));
+      if (a.n_states) a.n_states[e] = (int)(n > 0x7fffffffLL ? 0x7fffffffLL : n);
+      if (a.blocks) a.blocks[e] = (int)blocks;
+    }}
+  }}
+}}
+"""
+    for prune in (0, 1):
+        for staged in (0, 1):
+            for stop in (0, 1):
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
+                        f'vmp_validate_p{prune}_s{stop}_g{staged}(VmpValidateArgs a) '
+                        f'{{ vmp_validate_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
+            for stop in (1, 2):
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
+                        f'vmp_motion_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '
+                        f'{{ vmp_motion_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
+    return src
+
+
+def generate_source(program, pairs=None, name: str = "robot") -> str:
+    """Complete NVRTC translation unit for one robot (self-contained)."""
+    lay = derive_layout(program, pairs)
+    abi = (CSRC / "vmp_abi.h").read_text()
+    dev = (CSRC / "vmp_device.cuh").read_text()
+    fk = _fk_lines(program)
+    fk_macro = " \\\n  ".join(fk) if fk else ""
+    const_defs = []
+    values = np.asarray(program.values)
+    for s in lay.const_spheres:
+        for axis, op in zip("XYZ", s.xyz):
+            const_defs.append(f"#define VMP_C{s.slot}{axis} {f32_literal(values[op])}")
+    parts = [
+        f"// generated by paper_2309_14545_b200.codegen v{CODEGEN_VERSION}",
+        f"// dof={lay.dof} ops={lay.n_ops} markers={lay.n_markers} fine={len(lay.fine)} "
+        f"const={len(lay.const_spheres)} pairs={len(lay.pairs)}",
+        abi, dev,
+        f"#define VMP_FK_BODY \\\n  {fk_macro}",
+        "\n".join(const_defs),
+    ]
+    if lay.has_cc:
+        parts.append(_const_check(lay))
+        parts.append(_state_function(lay))
+    parts.append(_kernels(lay, program))
+    return "\n".join(parts) + "\n"
+
+
+def source_key(source: str) -> str:
+    return hashlib.sha256(source.encode()).hexdigest()[:24]
+
+
+def algorithmic_flops(program, pairs, counts) -> dict:
+    """Reference dense work per configuration.
+
+    F = #MUL + #ADD + #SUB  +  N_fine * (8 ks + 20 kc + 26 kb)  +  8 * N_pairs
+    (NEG and sin/cos not counted; coarse tests are pruning overhead).
+    """
+    kinds = np.asarray(program.kinds)
+    f_fk = int(np.sum((kinds == MUL) | (kinds == ADD) | (kinds == SUB)))
+    lay = derive_layout(program, pairs)
+    ks, kc, kb = counts
+    n_fine = len(lay.fine)
+    f_env = n_fine * (8 * ks + 20 * kc + 26 * kb)
+    f_self = 8 * len(lay.pairs)
+    return {"fk": f_fk, "env": f_env, "self": f_self, "total": f_fk + f_env + f_self,
+            "n_fine": n_fine, "n_pairs": len(lay.pairs),
+            "n_const_fine": len(lay.const_spheres)}

@@ -1,0 +1,216 @@
+/* Device helpers shared by every vmp kernel (sm_100a).
+ *
+ * - environment staging: one cp.async.bulk (UBLKCP) global->shared copy per
+ *   CTA, completed on an mbarrier, overlapped with the forward kinematics;
+ * - narrowphase tests in expanded FFMA form (one test = 5 / 12 / 16 issue
+ *   slots for sphere / capsule / cuboid obstacles);
+ * - exact-rounding motion helpers reproducing numpy float32 semantics
+ *   (reference lanes.py:91-113, motion.py:25-29,69-70).
+ *
+ * This file is inlined into NVRTC sources by codegen.py, so it may only use
+ * builtins (no system headers).
+ */
+#ifndef VMP_DEVICE_CUH
+#define VMP_DEVICE_CUH
+
+#define VMP_FULL 0xffffffffu
+
+/* ---------------------------------------------------------------- staging */
+
+__device__ __forceinline__ unsigned vmp_smem_addr(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void vmp_mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(vmp_smem_addr(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void vmp_bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                             unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(vmp_smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          vmp_smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(vmp_smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void vmp_mbar_wait(unsigned long long *bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(vmp_smem_addr(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+/* Stage the packed environment into shared memory (thread 0 issues one bulk
+ * copy).  Returns the pointer kernels should read records from.  Callers must
+ * vmp_mbar_wait(bar, 0) before the first dereference when staged. */
+__device__ __forceinline__ const float4 *vmp_env_begin(const VmpEnvView &env, int stage,
+                                                       float4 *smem,
+                                                       unsigned long long *bar) {
+  if (!stage || env.n_f4 == 0) return env.rec;
+  if (threadIdx.x == 0) {
+    vmp_mbar_init(bar, 1);
+    vmp_bulk_g2s(smem, env.rec, (unsigned)env.n_f4 * 16u, bar);
+  }
+  return smem;
+}
+
+/* ------------------------------------------------------------- narrowphase
+ * Records (float4 units), built on the host by vmp_env_create (vmp.cu):
+ *   sphere  k: R0 = (-2 o, -( |o|^2 - r^2 )),  R1 = (r, 0, 0, 0)
+ *   capsule k: R0 = (a, -p0.a), R1 = (-2 p0, -( |p0|^2 - r^2 )), R2 = (1/|a|^2, |a|^2, r, 0)
+ *   cuboid  k: R0..R2 = (row i of R^T, -(R^T c)_i),  R3 = (h, 0)
+ * For a robot sphere with centre c and radius rs, S = |c|^2 - rs^2 and
+ *   |c - o|^2 - (r + rs)^2 = S + r (-2 rs) + (-2 o).c + (|o|^2 - r^2)
+ * so the sphere test is 4 FFMA + 1 FSETP.  Hit <=> value <= 0, i.e. boundary
+ * contact counts as collision (reference collision.py:5-6, 206-211).
+ */
+
+__device__ __forceinline__ float vmp_sphere_S(float x, float y, float z, float rs2) {
+  return fmaf(x, x, fmaf(y, y, fmaf(z, z, -rs2)));
+}
+
+/* true = clear (no contact) */
+__device__ __forceinline__ bool vmp_clear_sphere(float x, float y, float z, float S, float m2rs,
+                                                 float4 r0, float r) {
+  float w = fmaf(r, m2rs, S);
+  w = fmaf(x, r0.x, w);
+  w = fmaf(y, r0.y, w);
+  w = fmaf(z, r0.z, w);
+  return w > r0.w;
+}
+
+__device__ __forceinline__ bool vmp_clear_capsule(float x, float y, float z, float S, float m2rs,
+                                                  float4 r0, float4 r1, float4 r2) {
+  float u = fmaf(x, r0.x, fmaf(y, r0.y, fmaf(z, r0.z, r0.w)));  /* (c - p0).a */
+  float t = __saturatef(u * r2.x);                                /* clamp(u / |a|^2, 0, 1) */
+  float w = fmaf(r2.z, m2rs, S);
+  w = fmaf(x, r1.x, w);
+  w = fmaf(y, r1.y, w);
+  w = fmaf(z, r1.z, w);                                            /* |c - p0|^2 - thr - A */
+  float v = fmaf(u, -2.0f, t * r2.y);                              /* t |a|^2 - 2 u */
+  float e = fmaf(t, v, w);                                         /* |c - p0 - t a|^2 - thr - A */
+  return e > r1.w;
+}
+
+/* rs < 1: |l| - h saturated to [0, 1] is exact below 1 and >= rs^2 above, so
+ * FADD.SAT replaces FADD + FMNMX without changing any verdict. */
+__device__ __forceinline__ bool vmp_clear_box_small(float x, float y, float z, float rs2,
+                                                    float4 r0, float4 r1, float4 r2, float4 r3) {
+  float l0 = fmaf(x, r0.x, fmaf(y, r0.y, fmaf(z, r0.z, r0.w)));
+  float l1 = fmaf(x, r1.x, fmaf(y, r1.y, fmaf(z, r1.z, r1.w)));
+  float l2 = fmaf(x, r2.x, fmaf(y, r2.y, fmaf(z, r2.z, r2.w)));
+  float e0 = __saturatef(fabsf(l0) - r3.x);
+  float e1 = __saturatef(fabsf(l1) - r3.y);
+  float e2 = __saturatef(fabsf(l2) - r3.z);
+  float d = fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
+  return d > rs2;
+}
+
+__device__ __forceinline__ bool vmp_clear_box_any(float x, float y, float z, float rs2,
+                                                  float4 r0, float4 r1, float4 r2, float4 r3) {
+  float l0 = fmaf(x, r0.x, fmaf(y, r0.y, fmaf(z, r0.z, r0.w)));
+  float l1 = fmaf(x, r1.x, fmaf(y, r1.y, fmaf(z, r1.z, r1.w)));
+  float l2 = fmaf(x, r2.x, fmaf(y, r2.y, fmaf(z, r2.z, r2.w)));
+  float e0 = fmaxf(fabsf(l0) - r3.x, 0.0f);
+  float e1 = fmaxf(fabsf(l1) - r3.y, 0.0f);
+  float e2 = fmaxf(fabsf(l2) - r3.z, 0.0f);
+  float d = fmaf(e0, e0, fmaf(e1, e1, e2 * e2));
+  return d > rs2;
+}
+
+__device__ __forceinline__ bool vmp_clear_box(float x, float y, float z, float rs, float rs2,
+                                              float4 r0, float4 r1, float4 r2, float4 r3) {
+  return rs < 1.0f ? vmp_clear_box_small(x, y, z, rs2, r0, r1, r2, r3)
+                   : vmp_clear_box_any(x, y, z, rs2, r0, r1, r2, r3);
+}
+
+/* Self pair: clear iff d^2 > f32(ra + rb)^2 (reference collision.py:385-394). */
+__device__ __forceinline__ bool vmp_clear_pair(float ax, float ay, float az, float bx, float by,
+                                               float bz, float thr) {
+  float dx = ax - bx, dy = ay - by, dz = az - bz;
+  return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) > thr;
+}
+
+/* Test one robot sphere against every obstacle of env (generic path used by
+ * the constant-sphere precheck and the single-primitive API wrappers). */
+__device__ __forceinline__ bool vmp_sphere_clear_env(const float4 *rec, int ns, int nc, int nb,
+                                                     float x, float y, float z, float rs) {
+  const float rs2 = rs * rs;
+  const float m2rs = -2.0f * rs;
+  const float S = vmp_sphere_S(x, y, z, rs2);
+  bool ok = true;
+  const float4 *p = rec;
+  for (int k = 0; k < ns; ++k, p += 2) ok &= vmp_clear_sphere(x, y, z, S, m2rs, p[0], p[1].x);
+  for (int k = 0; k < nc; ++k, p += 3) ok &= vmp_clear_capsule(x, y, z, S, m2rs, p[0], p[1], p[2]);
+  for (int k = 0; k < nb; ++k, p += 4) ok &= vmp_clear_box(x, y, z, rs, rs2, p[0], p[1], p[2], p[3]);
+  return ok;
+}
+
+/* ------------------------------------------------------- motion arithmetic */
+
+/* numpy float32 sum of squares of (a - b): sequential below 8 elements,
+ * eight interleaved accumulators combined as ((0+1)+(2+3))+((4+5)+(6+7)) plus
+ * a sequential tail from 8 upwards (numpy pairwise_sum, n <= 128). */
+template <int D>
+__device__ __forceinline__ float vmp_np_sumsq(const float *a, const float *b) {
+  float sq[D > 0 ? D : 1];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    float d = __fsub_rn(a[i], b[i]);
+    sq[i] = __fmul_rn(d, d);
+  }
+  if (D < 8) {
+    float r = 0.0f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) r = __fadd_rn(r, sq[i]);
+    return r;
+  } else {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = sq[j < D ? j : 0];
+    int i = 8;
+#pragma unroll
+    for (; i < D - (D % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], sq[(i + j) < D ? (i + j) : 0]);
+    }
+    float r = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3])),
+                        __fadd_rn(__fadd_rn(acc[4], acc[5]), __fadd_rn(acc[6], acc[7])));
+#pragma unroll
+    for (int t = D - (D % 8); t < D; ++t) r = __fadd_rn(r, sq[t]);
+    return r;
+  }
+}
+
+/* n = max(1, ceil(f64(sqrt_f32(sum)) / resolution))  (reference motion.py:25-29). */
+template <int D>
+__device__ __forceinline__ long long vmp_discretize(const float *s, const float *g, double res) {
+  float dist = __fsqrt_rn(vmp_np_sumsq<D>(s, g));
+  double steps = ceil(__ddiv_rn((double)dist, res));
+  long long n = (long long)steps;
+  return n < 1 ? 1 : n;
+}
+
+/* t = f32(f64(i) / n); q = s + t (g - s), unfused (reference motion.py:69-70,
+ * lanes.py:101). */
+__device__ __forceinline__ float vmp_rake_param(long long i, long long n) {
+  return __double2float_rn(__ddiv_rn((double)i, (double)n));
+}
+
+__device__ __forceinline__ float vmp_lerp_exact(float s, float g, float t) {
+  return __fadd_rn(s, __fmul_rn(t, __fsub_rn(g, s)));
+}
+
+#endif

@@ -1,0 +1,281 @@
+"""GPU parity: the sm_100a kernels (through the C ABI / reference-signature
+shims) against the pinned oracle and the reference's own golden outputs.
+
+Bars (BASELINE.json north_star):
+  * sphere centres within 1e-5 m of the float64 values;
+  * collision verdicts bit-identical for every configuration whose |minimum
+    signed clearance| > 1e-4 m; mismatches inside the band are counted;
+  * motion verdicts identical under the same resolution rule (and the
+    reference's rake block counts reproduced for the context width).
+"""
+
+import numpy as np
+import pytest
+
+import golden_io
+import vecmp_oracle as O
+from paper_2309_14545_b200 import (ConfigBlock, Scratch, ValidationContext, evaluate_program,
+                                   load_robot, soa_from_aos, validate_block, workloads)
+from paper_2309_14545_b200 import motion as M
+from paper_2309_14545_b200 import runtime
+
+pytestmark = pytest.mark.gpu
+
+ROBOTS = ("planar2", "arm7", "fetch_standin", "baxter_standin")
+BAND = 1e-4
+CENTRE_TOL = 1e-5
+
+
+def _verdict_parity(rob, prims, q, got):
+    """Assert bit-identical verdicts outside the band; return in-band mismatch count."""
+    ref = O.validate_configs(rob.program, rob.pairs, prims, q)
+    clear = O.clearance_f64(rob.program, rob.pairs, prims, q)
+    outside = np.abs(clear) > BAND
+    bad = np.flatnonzero(outside & (got != ref))
+    assert bad.size == 0, f"{bad.size} verdicts differ outside the band, e.g. {bad[:5]}"
+    return int(np.sum(~outside & (got != ref)))
+
+
+# ------------------------------------------------------------------ FK
+
+@pytest.mark.parametrize("name", ROBOTS)
+def test_fk_centres_within_1e5_of_float64(cuda, name):
+    fk = golden_io.load("fk")
+    rob = load_robot(name)
+    q = fk[f"q_{name}"]
+    cen = runtime.fk_spheres(rob.program, q).cpu().numpy().reshape(-1, 3, q.shape[1])
+    assert np.max(np.abs(cen - fk[f"f64_{name}"])) <= CENTRE_TOL
+    # and close to the reference's own float32 stream
+    assert np.max(np.abs(cen - fk[f"f32_{name}"])) <= CENTRE_TOL
+
+
+@pytest.mark.parametrize("name", ROBOTS)
+def test_fk_large_batch_vs_float64(cuda, name):
+    rob = load_robot(name)
+    q = workloads.uniform_configs(rob.limits, 100_000, 7)
+    cen = runtime.fk_spheres(rob.program, q).cpu().numpy().reshape(-1, 3, q.shape[1])
+    ref = O.marker_centres(rob.program, O.rows_f64(rob.program, q))
+    assert np.max(np.abs(cen - ref)) <= CENTRE_TOL
+
+
+def test_evaluate_program_sink_and_rows(cuda):
+    rob = load_robot("arm7")
+    rng = np.random.default_rng(31)
+    configs = [rng.uniform(rob.limits[:, 0], rob.limits[:, 1]).astype(np.float32) for _ in range(8)]
+
+    class Rec:
+        def __init__(self, stop=None):
+            self.calls, self.stop = [], stop
+
+        def __call__(self, m, x, y, z):
+            self.calls.append((m, x.copy(), y.copy(), z.copy()))
+            return self.stop is not None and len(self.calls) >= self.stop
+
+    wide = Rec()
+    scratch = evaluate_program(rob.program, soa_from_aos(configs, width=8), wide)
+    assert isinstance(scratch, Scratch) and scratch.rows.shape == (len(rob.program), 8)
+    assert len(wide.calls) == len(rob.program.checks)
+    for k, q in enumerate(configs):            # lanes == width-1 runs, bitwise
+        narrow = Rec()
+        evaluate_program(rob.program, soa_from_aos([q], width=1), narrow)
+        for (mw, xw, yw, zw), (mn, xn, yn, zn) in zip(wide.calls, narrow.calls):
+            assert mw is mn and xw[k] == xn[0] and yw[k] == yn[0] and zw[k] == zn[0]
+    partial = Rec(stop=3)
+    evaluate_program(rob.program, soa_from_aos(configs, width=8), partial)
+    assert len(partial.calls) == 3
+    with pytest.raises(ValueError):
+        evaluate_program(rob.program, soa_from_aos([np.zeros(3, np.float32)]), None)
+
+
+# ------------------------------------------------------------- blocks
+
+def _block_cases():
+    fx = golden_io.load("blocks")
+    for name in ROBOTS:
+        e = 0
+        while f"env_{name}_{e}_kinds" in fx:
+            yield name, e
+            e += 1
+
+
+@pytest.mark.parametrize("name,e", list(_block_cases()))
+def test_validate_block_vs_reference_goldens(cuda, name, e):
+    fx = golden_io.load("blocks")
+    rob = load_robot(name)
+    env = golden_io.env_from(fx, f"env_{name}_{e}")
+    q = fx[f"q_{name}"]
+    n = q.shape[1]
+    clear = O.clearance_f64(rob.program, rob.pairs, env.primitives, q)
+    outside = np.abs(clear) > BAND
+    for prune in (True, False):
+        ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=8, prune=prune)
+        got = np.concatenate([ctx.validate_block(ConfigBlock(rob.tree.dof, 8,
+                                                             np.ascontiguousarray(q[:, i:i + 8]), 8))
+                              for i in range(0, n, 8)])
+        ref = fx[f"v_{name}_{e}_w8_p{int(prune)}"]
+        assert np.array_equal(got[outside], ref[outside])
+        assert ctx.blocks_evaluated == n // 8
+    wide = validate_block(rob.program, rob.model, rob.pairs, env,
+                          ConfigBlock(rob.tree.dof, n, q, n))
+    assert np.array_equal(wide[outside], fx[f"v_{name}_{e}_wide"][outside])
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=8)
+    strict = np.concatenate([ctx.validate_block(ConfigBlock(rob.tree.dof, 8,
+                                                            np.ascontiguousarray(q[:, i:i + 8]), 8),
+                                                reject_all=True) for i in range(0, n, 8)])
+    blk_out = outside.reshape(-1, 8).all(axis=1).repeat(8)
+    assert np.array_equal(strict[blk_out], fx[f"v_{name}_{e}_reject_all"][blk_out])
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg3", "cfg4", "cfg5_16", "cfg5_128", "cfg5_1024"])
+def test_batch_workloads_vs_oracle(cuda, cfg):
+    n = 65536 if cfg == "cfg1" else 16384
+    wl = {"cfg1": lambda: workloads.config1(n), "cfg3": lambda: workloads.config3(n),
+          "cfg4": lambda: workloads.config4(n)}.get(cfg, lambda: workloads.config5(n, int(cfg[5:])))()
+    rob = load_robot(wl.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    got = ctx.validate_configs(wl.q)
+    band = _verdict_parity(rob, wl.env.primitives, wl.q, got)
+    assert band <= max(2, n // 2000)
+    rate = 1 - got.mean()
+    assert 0.15 < rate < 0.65, f"collision rate {rate:.3f} outside the calibrated band"
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4"])
+def test_full_size_batches_self_consistent(cuda, cfg):
+    """1M-config batches: size-independent properties (the oracle checks a sample)."""
+    torch = cuda
+    wl = workloads.config3() if cfg == "cfg3" else workloads.config4()
+    rob = load_robot(wl.robot)
+    n = wl.q.shape[1]
+    qd = torch.from_numpy(wl.q).cuda()
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    early = ctx.validate_batch(qd).cpu().numpy()
+    dense = ctx.validate_batch(qd, early_exit=False).cpu().numpy()
+    assert np.array_equal(early, dense)                      # early exit never changes verdicts
+    noprune = ValidationContext(rob.program, rob.model, rob.pairs, wl.env, prune=False)
+    assert np.array_equal(noprune.validate_batch(qd).cpu().numpy(), early)   # prune is sound
+    # chunked launches with a leading dimension == one launch
+    half = n // 2 + 17
+    a = runtime.unpack_bits(ctx.validate_batch(qd[:, :half]).cpu().numpy(), half)
+    b = runtime.unpack_bits(ctx.validate_batch(qd[:, half:]).cpu().numpy(), n - half)
+    full = runtime.unpack_bits(early, n)
+    assert np.array_equal(np.concatenate([a, b]), full)
+    idx = np.random.default_rng(5).choice(n, 8192, replace=False)
+    _verdict_parity(rob, wl.env.primitives, wl.q[:, idx], full[idx])
+
+
+def test_padding_permutation_and_edges(cuda):
+    rob = load_robot("arm7")
+    env = workloads.config2_scene()
+    rng = np.random.default_rng(61)
+    configs = [rng.uniform(rob.limits[:, 0], rob.limits[:, 1]).astype(np.float32) for _ in range(8)]
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env)
+    base = ctx.validate_block(soa_from_aos(configs, width=8))
+    perm = rng.permutation(8)
+    assert np.array_equal(ctx.validate_block(soa_from_aos([configs[p] for p in perm])), base[perm])
+    one = ctx.validate_block(soa_from_aos(configs[:3], width=8))[:3]
+    assert np.array_equal(one, base[:3])
+    assert ctx.state_valid(configs[0]) == bool(base[0])
+    from paper_2309_14545_b200 import Environment, SphereObstacle
+    empty = ValidationContext(rob.program, rob.model, rob.pairs, Environment())
+    assert empty.validate_configs(np.zeros((7, 5), np.float32)).all()
+    engulf = ValidationContext(rob.program, rob.model, rob.pairs,
+                               Environment([SphereObstacle(np.zeros(3), 5.0)]))
+    assert not engulf.validate_configs(np.zeros((7, 100), np.float32)).any()
+    assert engulf.validate_configs(np.zeros((7, 0), np.float32)).size == 0
+
+
+# ---------------------------------------------------------- narrowphase
+
+def test_single_obstacle_lane_wrappers_vs_reference(cuda):
+    from paper_2309_14545_b200 import (BoxObstacle, CapsuleObstacle, SphereObstacle,
+                                       sphere_vs_capsule_lanes, sphere_vs_cuboid_lanes,
+                                       sphere_vs_sphere_lanes)
+    N = golden_io.load("narrow")
+    mism = 0
+    for i in range(0, len(N["sph_r"]), 3):
+        h = sphere_vs_sphere_lanes(*N["sph_pts"][i].T, float(N["sph_rs"][i]),
+                                   SphereObstacle(N["sph_c"][i], float(N["sph_r"][i])))
+        mism += int(np.sum(h != N["sph_hits"][i]))
+    for i in range(0, len(N["cap_r"]), 3):
+        h = sphere_vs_capsule_lanes(*N["cap_pts"][i].T, float(N["cap_rs"][i]),
+                                    CapsuleObstacle(N["cap_p0"][i], N["cap_p1"][i], float(N["cap_r"][i])))
+        mism += int(np.sum(h != N["cap_hits"][i]))
+    for i in list(range(50)) + list(range(50, len(N["box_rs"]), 3)):
+        h = sphere_vs_cuboid_lanes(*N["box_pts"][i].T, float(N["box_rs"][i]),
+                                   BoxObstacle(N["box_c"][i], N["box_h"][i], N["box_rot"][i]))
+        mism += int(np.sum(h != N["box_hits"][i]))
+    assert mism == 0
+
+
+# --------------------------------------------------------------- motion
+
+def _motion_keys():
+    fx = golden_io.load("motion")
+    return sorted({k[len("starts_"):] for k in fx.files if k.startswith("starts_")})
+
+
+@pytest.mark.parametrize("key", _motion_keys())
+def test_rake_vs_reference_goldens(cuda, key):
+    fx = golden_io.load("motion")
+    rob = load_robot(key.rsplit("_", 1)[0])
+    env = golden_io.env_from(fx, f"env_{key}")
+    s, g, res = fx[f"starts_{key}"], fx[f"goals_{key}"], float(fx[f"res_{key}"])
+    ns = [M.discretization_count(a, b, res) for a, b in zip(s[:20], g[:20])]
+    assert ns == fx[f"n_{key}"][:20].tolist()
+    for width in (8, 1, 32):
+        for bwd in (0, 1):
+            tag = f"{key}_w{width}_b{bwd}"
+            ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=width)
+            bits, n_states, blocks = M.validate_motions(ctx, s, g, res, backward=bool(bwd),
+                                                        width=width, counts=True)
+            verdict = runtime.unpack_bits(bits.cpu().numpy(), len(s))
+            assert verdict.tolist() == fx[f"verdict_{tag}"].tolist()
+            assert blocks.cpu().numpy().tolist() == fx[f"blocks_{tag}"].tolist()
+            assert n_states.cpu().numpy().tolist() == fx[f"n_{key}"].tolist()
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=8)
+    for i in range(0, len(s), 9):                       # the per-edge shim, too
+        assert M.raked_motion_check(s[i], g[i], ctx, res) == (
+            bool(fx[f"verdict_{key}_w8_b0"][i]), int(fx[f"blocks_{key}_w8_b0"][i]))
+
+
+def test_cfg2_all_edges_vs_oracle(cuda):
+    mw = workloads.config2()
+    rob = load_robot("arm7")
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    bits, n_states, blocks = M.validate_motions(ctx, mw.starts, mw.goals, mw.resolution, counts=True)
+    verdict = runtime.unpack_bits(bits.cpu().numpy(), len(mw.starts))
+    ob = O.Obstacles(mw.env.primitives)
+    expect, ns = [], []
+    for a, b in zip(mw.starts, mw.goals):
+        n, v = O.edge_all_states(rob.program, rob.pairs, ob, a, b, mw.resolution)
+        expect.append(bool(v.all()))
+        ns.append(n)
+    assert n_states.cpu().numpy().tolist() == ns
+    assert verdict.tolist() == expect
+    assert verdict[0::2].all()                         # forced-free edges
+    assert 0.4 < verdict.mean() < 0.7
+
+
+def test_discretize_bitwise_vs_reference(cuda):
+    L = golden_io.load("lanes")
+    for d in range(1, 17):
+        a, b = L[f"a_{d}"], L[f"b_{d}"]
+        for tag, res in (("r32", 1.0 / 32.0), ("r05", 0.05), ("r07", 0.07)):
+            got = runtime.discretize_device(runtime.to_device(a), runtime.to_device(b), res)
+            assert got.cpu().numpy().tolist() == L[f"n_{tag}_{d}"].tolist()
+
+
+def test_motion_errors(cuda):
+    rob = load_robot("planar2")
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, workloads.config2_scene())
+    with pytest.raises(ValueError):
+        M.raked_motion_check(np.zeros(2, np.float32), np.ones(2, np.float32), ctx, 0.0)
+    with pytest.raises(ValueError):
+        M.raked_motion_check(np.zeros(2, np.float32), np.ones(3, np.float32), ctx, 0.1)
+    with pytest.raises(ValueError):
+        M.discretization_count(np.zeros(2), np.ones(2), -1.0)
+    q = np.array([0.5, -0.5], np.float32)
+    from paper_2309_14545_b200 import Environment
+    free = ValidationContext(rob.program, rob.model, rob.pairs, Environment())
+    assert M.raked_motion_check(q, q, free, 0.05) == (True, 1)
