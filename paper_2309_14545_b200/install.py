@@ -1,0 +1,72 @@
+"""Drop the B200 path into an imported reference package (``vecmp``).
+
+    import vecmp
+    from paper_2309_14545_b200.install import patch_vecmp
+    patch_vecmp(vecmp)
+
+Rebinds the hot-path names everywhere the reference binds them - its own
+modules import them by value at import time (planners.py:18,21,
+simplify.py:17,19, cli.py:22,24) - so the reference's
+planners, simplifier, CLI/RPC and tests run their FK, collision checks and
+motion validation on the GPU.  Host-side types (ConfigBlock, Environment,
+primitives, KinematicProgram) stay the reference's own; the shims duck-type
+them.  ``unpatch`` restores the originals.
+"""
+
+from __future__ import annotations
+
+import importlib
+
+from . import collision, motion, program
+
+#: module -> names to rebind (only where the module actually defines them)
+TARGETS = {
+    "": ("evaluate_program", "validate_block", "ValidationContext", "sphere_vs_sphere_lanes",
+         "sphere_vs_capsule_lanes", "sphere_vs_cuboid_lanes", "discretization_count",
+         "raked_motion_check", "validate_motion_rake"),
+    "program": ("evaluate_program",),
+    "collision": ("evaluate_program", "validate_block", "ValidationContext",
+                  "sphere_vs_sphere_lanes", "sphere_vs_capsule_lanes", "sphere_vs_cuboid_lanes"),
+    "motion": ("ValidationContext", "discretization_count", "raked_motion_check",
+               "validate_motion_rake"),
+    "planners": ("ValidationContext", "validate_motion_rake"),
+    "simplify": ("ValidationContext", "validate_motion_rake"),
+    "cli": ("ValidationContext", "validate_motion_rake"),
+}
+
+REPLACEMENTS = {
+    "evaluate_program": program.evaluate_program,
+    "validate_block": collision.validate_block,
+    "ValidationContext": collision.ValidationContext,
+    "sphere_vs_sphere_lanes": collision.sphere_vs_sphere_lanes,
+    "sphere_vs_capsule_lanes": collision.sphere_vs_capsule_lanes,
+    "sphere_vs_cuboid_lanes": collision.sphere_vs_cuboid_lanes,
+    "discretization_count": motion.discretization_count,
+    "raked_motion_check": motion.raked_motion_check,
+    "validate_motion_rake": motion.validate_motion_rake,
+}
+
+_SAVED: dict = {}
+
+
+def patch_vecmp(pkg) -> list[str]:
+    """Rebind the hot-path names in ``pkg`` (the imported vecmp package)."""
+    done = []
+    for sub, names in TARGETS.items():
+        try:
+            mod = importlib.import_module(f"{pkg.__name__}.{sub}") if sub else pkg
+        except ImportError:
+            continue
+        for name in names:
+            if hasattr(mod, name):
+                _SAVED.setdefault((mod.__name__, name), getattr(mod, name))
+                setattr(mod, name, REPLACEMENTS[name])
+                done.append(f"{mod.__name__}.{name}")
+    return done
+
+
+def unpatch_vecmp(pkg) -> None:
+    for (modname, name), original in list(_SAVED.items()):
+        mod = importlib.import_module(modname)
+        setattr(mod, name, original)
+    _SAVED.clear()

@@ -35,6 +35,12 @@ def _pair(start: Config, goal: Config) -> tuple[np.ndarray, np.ndarray]:
     return s, g
 
 
+def _bind(ctx):
+    """(robot module, device env) for any context exposing program/pairs/env
+    (ours, or a reference ValidationContext built before patch_vecmp)."""
+    return (runtime.robot_module(ctx.program, ctx.pairs), runtime.device_env(ctx.env))
+
+
 def _check_resolution(resolution: float) -> None:
     if not resolution > 0:
         raise ValueError(f"resolution must be positive, got {resolution}")
@@ -67,8 +73,8 @@ def raked_motion_check(start: Config, goal: Config, ctx: ValidationContext,
     sd = runtime.to_device(s.reshape(1, -1))
     gd = runtime.to_device(g.reshape(1, -1))
     bits, _, blocks = runtime.validate_motions_device(
-        ctx.module, ctx.device_env, sd, gd, resolution, width=ctx.width, backward=backward,
-        prune=ctx.prune, want_counts=True)
+        *_bind(ctx), sd, gd, resolution, width=ctx.width, backward=backward,
+        prune=getattr(ctx, "prune", True), want_counts=True)
     verdict = bool(int(bits[0].item()) & 1)
     nblocks = int(blocks[0].item())
     ctx.blocks_evaluated += nblocks
@@ -102,6 +108,6 @@ def validate_motions(ctx: ValidationContext, starts, goals, resolution: float, *
     gd = gd.contiguous()
     ctx.motion_checks += sd.shape[0]
     b, n_states, blocks = runtime.validate_motions_device(
-        ctx.module, ctx.device_env, sd, gd, resolution, width=width, backward=backward,
-        prune=ctx.prune, want_counts=counts, bits=bits, workspace=workspace)
+        *_bind(ctx), sd, gd, resolution, width=width, backward=backward,
+        prune=getattr(ctx, "prune", True), want_counts=counts, bits=bits, workspace=workspace)
     return (b, n_states, blocks) if counts else b

@@ -176,8 +176,13 @@ def build_robot(tree: KinematicTree, model: SphereModel, ignore_pairs=None,
                  limits=tree.joint_limits(), name=name)
 
 
-@lru_cache(maxsize=None)
 def load_robot(name: str) -> Robot:
-    urdf, spheres = robot_texts(STANDIN_FOR.get(name, name))
+    """Compiled bundle of a known robot; BASELINE names map to their stand-ins."""
+    return _load(STANDIN_FOR.get(name, name))
+
+
+@lru_cache(maxsize=None)
+def _load(name: str) -> Robot:
+    urdf, spheres = robot_texts(name)
     tree = parse_urdf(urdf)
-    return build_robot(tree, load_sphere_model(tree, spheres), name=STANDIN_FOR.get(name, name))
+    return build_robot(tree, load_sphere_model(tree, spheres), name=name)
