@@ -145,7 +145,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     sd = torch.from_numpy(mw.starts).cuda()
     gd = torch.from_numpy(mw.goals).cuda()
     bits = torch.empty((E + 31) // 32, dtype=torch.int32, device="cuda")
-    ws = torch.empty(1, dtype=torch.int32, device="cuda")
+    ws = runtime.motion_workspace(E)
     n_states = torch.empty(E, dtype=torch.int32, device="cuda")
     blocks = torch.empty(E, dtype=torch.int32, device="cuda")
     mod, denv = ctx.module, ctx.device_env

@@ -100,14 +100,19 @@ int vmp_validate(const vmp_robot *robot, const vmp_env *env, const float *q, int
  * validate_motion_rake (reference motion.py:38-90) batched over edges.
  *   width      : rake width W whose block counts are reproduced (ctx.width);
  *                32 is the native warp width
- *   valid_bits : ceil(n_edges/32) words (zeroed by this call)
+ *   valid_bits : ceil(n_edges/32) words, bit set = every state valid
  *   n_states   : optional, discretization_count per edge (motion.py:25-29)
  *   blocks     : optional, block evaluations the W-wide rake performs
- *   workspace  : >= 4 bytes of device scratch (persistent work queue) */
+ *   workspace  : >= vmp_motion_workspace_bytes(n_edges) bytes of device
+ *                scratch (work queue + per-edge plan); 16-byte aligned
+ * Launches plan -> fused FK+CC rake -> finalize on `stream`. */
 int vmp_validate_motions(const vmp_robot *robot, const vmp_env *env, const float *starts,
                          const float *goals, int64_t n_edges, int64_t sld, double resolution,
                          int32_t width, uint32_t flags, uint32_t *valid_bits, int32_t *n_states,
-                         int32_t *blocks, void *workspace, void *stream);
+                         int32_t *blocks, void *workspace, int64_t workspace_bytes, void *stream);
+
+/* Device scratch bytes vmp_validate_motions needs for n_edges edges. */
+int64_t vmp_motion_workspace_bytes(int64_t n_edges);
 
 /* n = max(1, ceil(||g - s|| / resolution)) per edge with numpy float32
  * reduction order (reference motion.py:25-29, lanes.py:106-113). */

@@ -346,6 +346,11 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
 
 template <int PRUNE, int STOP, bool STAGED>
 __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
+  // Work items are (chunk c, edge e) pairs in c-major order; chunk c of an
+  // edge is rake positions [32c, 32c + 32) of the W-lane rake sequence
+  // (exactly one rake iteration when W = 32).  Warps grab 32 items per
+  // atomic, skip items of absent chunks or of edges already known to fail at
+  // an earlier iteration, and evaluate the rest one warp-wide chunk at a time.
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
   const float4 *env = a.env.rec;
@@ -358,49 +363,48 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
   const int lane = threadIdx.x & 31;
   const long long W = a.width;
+  const long long E = a.n_edges;
+  const long long total_items = (long long)__ldcg(&a.hdr->max_chunks) * E;
   for (;;) {{
-    unsigned e = 0;
-    if (lane == 0) e = atomicAdd(a.queue, 1u);
-    e = __shfl_sync(VMP_FULL, e, 0);
-    if ((long long)e >= a.n_edges) break;
-    float s[{dofp}], g[{dofp}];
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&a.hdr->counter, 32ull);
+    base = __shfl_sync(VMP_FULL, base, 0);
+    if ((long long)base >= total_items) break;
+    {{
+      const long long t = (long long)base + lane;
+      const long long c = t / E, e = t - c * E;
+      bool live = t < total_items && c < __ldg(a.chunks_of + e);
+      if (live) live = __ldcg(a.fail_of + e) > (int)((32 * c) / W + 1);
+      unsigned todo = __ballot_sync(VMP_FULL, live);
+      while (todo) {{
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const long long ti = (long long)base + src;
+        const long long ci = ti / E, ei = ti - ci * E;
+        const long long first_iter = (32 * ci) / W + 1;
+        if (__ldcg(a.fail_of + ei) <= (int)first_iter) continue;   // cannot lower the count
+        float s[{dofp}], g[{dofp}];
 #pragma unroll
-    for (int j = 0; j < {lay.dof}; ++j) {{
-      s[j] = __ldg(a.starts + (long long)e * a.sld + j);
-      g[j] = __ldg(a.goals + (long long)e * a.sld + j);
-    }}
-    const long long n = vmp_discretize<{lay.dof}>(s, g, a.resolution);
-    const long long S = (n + W - 1) / W;
-    const long long total = S * W;
-    bool verdict = true;
-    long long blocks = S;
-    if (!cclear) {{
-      verdict = false;
-      blocks = 1;
-    }} else {{
-      for (long long base = 0; base < total; base += 32) {{
-        const long long p = base + lane;
+        for (int j = 0; j < {lay.dof}; ++j) {{
+          s[j] = __ldg(a.starts + ei * a.sld + j);
+          g[j] = __ldg(a.goals + ei * a.sld + j);
+        }}
+        const long long n = __ldg(a.n_of + ei);
+        const long long S = (n + W - 1) / W;
+        const long long p = 32 * ci + lane;
         const long long j = p / W + 1;
         const long long k = p - (j - 1) * W;
         const long long idx = k * S + (a.backward ? (S - j + 1) : j);
-        const bool inr = p < total && idx <= n;
-        const float t = vmp_rake_param(inr ? idx : 1, n);
+        const bool inr = p < S * W && idx <= n;
+        const float tt = vmp_rake_param(inr ? idx : 1, n);
         float q[{dofp}];
 #pragma unroll
-        for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], t);
-        const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr);
+        for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
+        const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
         const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
-        if (bad) {{
-          verdict = false;
-          blocks = (base + __ffs(bad) - 1) / W + 1;
-          break;
-        }}
+        if (bad && lane == 0)
+          atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
       }}
-    }}
-    if (lane == 0) {{
-      if (verdict) atomicOr(a.bits + (e >> 5), 1u << (e & 31));
-      if (a.n_states) a.n_states[e] = (int)(n > 0x7fffffffLL ? 0x7fffffffLL : n);
-      if (a.blocks) a.blocks[e] = (int)blocks;
     }}
   }}
 }}

@@ -23,6 +23,13 @@ typedef struct {
   int pad_;
 } VmpValidateArgs;
 
+/* Motion workspace: this header, then int n[E], int chunks[E], int fail[E]. */
+typedef struct {
+  unsigned long long counter; /* work-item queue (zeroed before the plan kernel) */
+  unsigned int max_chunks;    /* max over edges of ceil(S W / 32), S = ceil(n / W) */
+  unsigned int pad_;
+} VmpMotionHeader;
+
 typedef struct {
   const float *starts; /* (n_edges, sld) float32 AoS */
   const float *goals;  /* (n_edges, sld) float32 AoS */
@@ -30,12 +37,12 @@ typedef struct {
   long long sld;       /* row stride of starts / goals in floats */
   double resolution;
   VmpEnvView env;
-  unsigned int *bits;  /* ceil(n_edges / 32) packed edge verdicts (pre-zeroed) */
-  int *n_states;       /* optional (may be NULL): discretisation count per edge */
-  int *blocks;         /* optional (may be NULL): rake iterations the reference would run */
-  unsigned int *queue; /* persistent work counter (pre-zeroed), one uint */
-  int width;           /* rake lane width W whose block counts are reproduced */
-  int backward;        /* comb strata top-down */
+  VmpMotionHeader *hdr;
+  const int *n_of;      /* discretisation count per edge (plan kernel) */
+  const int *chunks_of; /* 32-position chunks per edge (plan kernel) */
+  int *fail_of;         /* first failing rake iteration, INT_MAX while none */
+  int width;            /* rake lane width W whose block counts are reproduced */
+  int backward;         /* comb strata top-down */
   int stage;
   int pad_;
 } VmpMotionArgs;
