@@ -346,11 +346,13 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
 
 template <int PRUNE, int STOP, bool STAGED>
 __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
-  // Work items are (chunk c, edge e) pairs in c-major order; chunk c of an
-  // edge is rake positions [32c, 32c + 32) of the W-lane rake sequence
-  // (exactly one rake iteration when W = 32).  Warps grab 32 items per
-  // atomic, skip items of absent chunks or of edges already known to fail at
-  // an earlier iteration, and evaluate the rest one warp-wide chunk at a time.
+  // Work items are (chunk c, edge e) pairs enumerated round by round (c-major,
+  // dense: the plan kernels sort edges by chunk count so round c lists exactly
+  // the edges that have a chunk c).  Chunk c is rake positions [32c, 32c + 32)
+  // of the W-lane rake sequence - exactly one rake iteration when W = 32.
+  // One item per atomic keeps the work granularity at one warp-chunk, so the
+  // tail is one chunk long instead of a whole edge; items of edges already
+  // known to fail at an earlier iteration are skipped.
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
   const float4 *env = a.env.rec;
@@ -363,49 +365,53 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
   const int lane = threadIdx.x & 31;
   const long long W = a.width;
-  const long long E = a.n_edges;
-  const long long total_items = (long long)__ldcg(&a.hdr->max_chunks) * E;
+  const long long total_items = (long long)__ldcg(&a.hdr->total_items);
+  const long long split = __ldg(a.off + (VMP_HBINS - 1));
+  const long long n_big = __ldcg(&a.hdr->n_big);
   for (;;) {{
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(&a.hdr->counter, 32ull);
-    base = __shfl_sync(VMP_FULL, base, 0);
-    if ((long long)base >= total_items) break;
-    {{
-      const long long t = (long long)base + lane;
-      const long long c = t / E, e = t - c * E;
-      bool live = t < total_items && c < __ldg(a.chunks_of + e);
-      if (live) live = __ldcg(a.fail_of + e) > (int)((32 * c) / W + 1);
-      unsigned todo = __ballot_sync(VMP_FULL, live);
-      while (todo) {{
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const long long ti = (long long)base + src;
-        const long long ci = ti / E, ei = ti - ci * E;
-        const long long first_iter = (32 * ci) / W + 1;
-        if (__ldcg(a.fail_of + ei) <= (int)first_iter) continue;   // cannot lower the count
-        float s[{dofp}], g[{dofp}];
-#pragma unroll
-        for (int j = 0; j < {lay.dof}; ++j) {{
-          s[j] = __ldg(a.starts + ei * a.sld + j);
-          g[j] = __ldg(a.goals + ei * a.sld + j);
-        }}
-        const long long n = __ldg(a.n_of + ei);
-        const long long S = (n + W - 1) / W;
-        const long long p = 32 * ci + lane;
-        const long long j = p / W + 1;
-        const long long k = p - (j - 1) * W;
-        const long long idx = k * S + (a.backward ? (S - j + 1) : j);
-        const bool inr = p < S * W && idx <= n;
-        const float tt = vmp_rake_param(inr ? idx : 1, n);
-        float q[{dofp}];
-#pragma unroll
-        for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
-        const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
-        const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
-        if (bad && lane == 0)
-          atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
+    unsigned long long item = 0;
+    if (lane == 0) item = atomicAdd(&a.hdr->counter, 1ull);
+    const long long t = (long long)__shfl_sync(VMP_FULL, item, 0);
+    if (t >= total_items) break;
+    long long ci, ri;
+    if (t < split) {{                       // largest c with off[c] <= t
+      int lo = 0, hi = VMP_HBINS - 1;
+      while (hi - lo > 1) {{
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a.off + mid) <= t) lo = mid; else hi = mid;
       }}
+      ci = lo;
+      ri = t - __ldg(a.off + lo);
+    }} else {{                              // rounds beyond the histogram
+      const long long u = t - split;
+      ci = (VMP_HBINS - 1) + u / n_big;
+      ri = u - (ci - (VMP_HBINS - 1)) * n_big;
     }}
+    const long long ei = __ldg(a.order + ri);
+    if (ci >= __ldg(a.chunks_of + ei)) continue;
+    const long long first_iter = (32 * ci) / W + 1;
+    if (__ldcg(a.fail_of + ei) <= (int)first_iter) continue;   // cannot lower the count
+    float s[{dofp}], g[{dofp}];
+#pragma unroll
+    for (int j = 0; j < {lay.dof}; ++j) {{
+      s[j] = __ldg(a.starts + ei * a.sld + j);
+      g[j] = __ldg(a.goals + ei * a.sld + j);
+    }}
+    const long long n = __ldg(a.n_of + ei);
+    const long long S = (n + W - 1) / W;
+    const long long p = 32 * ci + lane;
+    const long long j = p / W + 1;
+    const long long k = p - (j - 1) * W;
+    const long long idx = k * S + (a.backward ? (S - j + 1) : j);
+    const bool inr = p < S * W && idx <= n;
+    const float tt = vmp_rake_param(inr ? idx : 1, n);
+    float q[{dofp}];
+#pragma unroll
+    for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
+    const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
+    const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
+    if (bad && lane == 0)
+      atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
   }}
 }}
 """

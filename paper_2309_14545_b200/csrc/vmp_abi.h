@@ -23,11 +23,21 @@ typedef struct {
   int pad_;
 } VmpValidateArgs;
 
-/* Motion workspace: this header, then int n[E], int chunks[E], int fail[E]. */
+/* Motion workspace (all zero-initialised by one memset, then the plan):
+ *   VmpMotionHeader
+ *   unsigned hist[VMP_HBINS], fill[VMP_HBINS]   chunk-count histogram / scatter cursors
+ *   long long off[VMP_HBINS]                    first work item of chunk round c
+ *   int n[E], chunks[E], fail[E], order[E]      per-edge plan, order = edges by chunks desc
+ * Work item t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c,
+ * where off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest
+ * edges (chunks >= HBINS-1) and skip absent chunks. */
+#define VMP_HBINS 1024
 typedef struct {
-  unsigned long long counter; /* work-item queue (zeroed before the plan kernel) */
-  unsigned int max_chunks;    /* max over edges of ceil(S W / 32), S = ceil(n / W) */
-  unsigned int pad_;
+  unsigned long long counter;     /* work-item queue */
+  unsigned long long total_items; /* written by the scan kernel */
+  unsigned int max_chunks;        /* max over edges of ceil(S W / 32), S = ceil(n / W) */
+  unsigned int n_big;             /* edges with chunks >= VMP_HBINS - 1 */
+  unsigned int pad_[2];
 } VmpMotionHeader;
 
 typedef struct {
@@ -38,9 +48,11 @@ typedef struct {
   double resolution;
   VmpEnvView env;
   VmpMotionHeader *hdr;
+  const long long *off; /* first work item of each chunk round */
   const int *n_of;      /* discretisation count per edge (plan kernel) */
   const int *chunks_of; /* 32-position chunks per edge (plan kernel) */
   int *fail_of;         /* first failing rake iteration, INT_MAX while none */
+  const int *order;     /* edges sorted by chunk count, descending */
   int width;            /* rake lane width W whose block counts are reproduced */
   int backward;         /* comb strata top-down */
   int stage;
