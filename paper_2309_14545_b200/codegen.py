@@ -368,50 +368,62 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   const long long total_items = (long long)__ldcg(&a.hdr->total_items);
   const long long split = __ldg(a.off + (VMP_HBINS - 1));
   const long long n_big = __ldcg(&a.hdr->n_big);
-  for (;;) {{
-    unsigned long long item = 0;
-    if (lane == 0) item = atomicAdd(&a.hdr->counter, 1ull);
-    const long long t = (long long)__shfl_sync(VMP_FULL, item, 0);
-    if (t >= total_items) break;
+  unsigned long long grab = 0;
+  if (lane == 0) grab = atomicAdd(&a.hdr->counter, 1ull);
+  long long t = (long long)__shfl_sync(VMP_FULL, grab, 0);
+  while (t < total_items) {{
+    if (lane == 0) grab = atomicAdd(&a.hdr->counter, 1ull);   // prefetch the next item
     long long ci, ri;
-    if (t < split) {{                       // largest c with off[c] <= t
-      int lo = 0, hi = VMP_HBINS - 1;
-      while (hi - lo > 1) {{
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(a.off + mid) <= t) lo = mid; else hi = mid;
-      }}
-      ci = lo;
-      ri = t - __ldg(a.off + lo);
-    }} else {{                              // rounds beyond the histogram
+    if (t < split) {{
+      ci = vmp_find_round(a.off, t, lane);
+      ri = t - __ldg(a.off + ci);
+    }} else {{                              // rounds beyond the histogram (very long edges)
       const long long u = t - split;
       ci = (VMP_HBINS - 1) + u / n_big;
       ri = u - (ci - (VMP_HBINS - 1)) * n_big;
     }}
     const long long ei = __ldg(a.order + ri);
-    if (ci >= __ldg(a.chunks_of + ei)) continue;
     const long long first_iter = (32 * ci) / W + 1;
-    if (__ldcg(a.fail_of + ei) <= (int)first_iter) continue;   // cannot lower the count
-    float s[{dofp}], g[{dofp}];
-#pragma unroll
-    for (int j = 0; j < {lay.dof}; ++j) {{
-      s[j] = __ldg(a.starts + ei * a.sld + j);
-      g[j] = __ldg(a.goals + ei * a.sld + j);
-    }}
+    const int chunks = __ldg(a.chunks_of + ei);
+    const int failed = __ldcg(a.fail_of + ei);
     const long long n = __ldg(a.n_of + ei);
-    const long long S = (n + W - 1) / W;
-    const long long p = 32 * ci + lane;
-    const long long j = p / W + 1;
-    const long long k = p - (j - 1) * W;
-    const long long idx = k * S + (a.backward ? (S - j + 1) : j);
-    const bool inr = p < S * W && idx <= n;
-    const float tt = vmp_rake_param(inr ? idx : 1, n);
-    float q[{dofp}];
+    if (ci < chunks && failed > (int)first_iter) {{   // else: absent, or cannot lower the count
+      float s[{dofp}], g[{dofp}];
 #pragma unroll
-    for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
-    const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
-    const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
-    if (bad && lane == 0)
-      atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
+      for (int j = 0; j < {lay.dof}; ++j) {{
+        s[j] = __ldg(a.starts + ei * a.sld + j);
+        g[j] = __ldg(a.goals + ei * a.sld + j);
+      }}
+      const long long S = (n + W - 1) / W;
+      const long long p = 32 * ci + lane;
+      const long long j = p / W + 1;
+      const long long k = p - (j - 1) * W;
+      const long long idx = k * S + (a.backward ? (S - j + 1) : j);
+      const bool inr = p < S * W && idx <= n;
+      const float tt = vmp_rake_param(inr ? idx : 1, n);
+      float q[{dofp}];
+#pragma unroll
+      for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
+      const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
+      const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
+      if (bad && lane == 0)
+        atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
+    }}
+    t = (long long)__shfl_sync(VMP_FULL, grab, 0);
+  }}
+  if (a.fused_finalize) {{                  // the last CTA to finish writes the outputs
+    __shared__ unsigned vmp_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {{
+      __threadfence();
+      vmp_last = atomicAdd(&a.hdr->done_ctas, 1u) == gridDim.x - 1;
+    }}
+    __syncthreads();
+    if (vmp_last) {{
+      __threadfence();
+      vmp_motion_outputs(a.n_edges, a.width, a.n_of, a.fail_of, a.bits, a.n_states, a.blocks,
+                         0, {BLOCK}, threadIdx.x);
+    }}
   }}
 }}
 """

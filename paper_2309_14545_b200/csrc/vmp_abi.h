@@ -37,7 +37,8 @@ typedef struct {
   unsigned long long total_items; /* written by the scan kernel */
   unsigned int max_chunks;        /* max over edges of ceil(S W / 32), S = ceil(n / W) */
   unsigned int n_big;             /* edges with chunks >= VMP_HBINS - 1 */
-  unsigned int pad_[2];
+  unsigned int done_ctas;         /* CTAs of the rake kernel that finished */
+  unsigned int pad_;
 } VmpMotionHeader;
 
 typedef struct {
@@ -53,10 +54,13 @@ typedef struct {
   const int *chunks_of; /* 32-position chunks per edge (plan kernel) */
   int *fail_of;         /* first failing rake iteration, INT_MAX while none */
   const int *order;     /* edges sorted by chunk count, descending */
+  unsigned int *bits;   /* outputs, written by the last CTA when fused_finalize */
+  int *n_states;
+  int *blocks;
   int width;            /* rake lane width W whose block counts are reproduced */
   int backward;         /* comb strata top-down */
   int stage;
-  int pad_;
+  int fused_finalize;   /* 1: the last CTA to finish writes the outputs */
 } VmpMotionArgs;
 
 typedef struct {

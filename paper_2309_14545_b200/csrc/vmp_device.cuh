@@ -213,4 +213,39 @@ __device__ __forceinline__ float vmp_lerp_exact(float s, float g, float t) {
   return __fadd_rn(s, __fmul_rn(t, __fsub_rn(g, s)));
 }
 
+/* Motion outputs from the per-edge plan: verdict bit (no failure recorded),
+ * n, and the W-rake block count (failing iteration, or S = ceil(n / W)).
+ * Threads [tid0, tid0 + nthreads) of a group; nthreads a multiple of 32. */
+__device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width, const int *n_of,
+                                                   const int *fail_of, unsigned *bits,
+                                                   int *n_states, int *blocks, long long tid0,
+                                                   long long nthreads, int tid) {
+  for (long long base = tid0; base < n_edges; base += nthreads) {
+    const long long e = base + tid;
+    const bool inr = e < n_edges;
+    const int fail = inr ? __ldcg(fail_of + e) : 0;
+    const bool ok = inr && fail == 0x7fffffff;
+    const unsigned m = __ballot_sync(VMP_FULL, ok);
+    if (inr) {
+      if ((tid & 31) == 0) bits[e >> 5] = m;
+      const long long n = n_of[e];
+      if (n_states) n_states[e] = (int)n;
+      if (blocks) blocks[e] = ok ? (int)((n + width - 1) / width) : fail;
+    }
+  }
+}
+
+/* Round c of the motion work list holding item t: the largest c with
+ * off[c] <= t, found 32 rounds per step with one load per lane + ballot. */
+__device__ __forceinline__ int vmp_find_round(const long long *off, long long t, int lane) {
+  int base = 0;
+  for (;;) {
+    const int c = base + lane;
+    const bool le = c < VMP_HBINS && __ldg(off + c) <= t;
+    const unsigned m = __ballot_sync(VMP_FULL, le);
+    if (m != VMP_FULL || base + 32 >= VMP_HBINS) return base + 31 - __clz(m);
+    base += 32;
+  }
+}
+
 #endif
