@@ -368,11 +368,19 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   const long long total_items = (long long)__ldcg(&a.hdr->total_items);
   const long long split = __ldg(a.off + (VMP_HBINS - 1));
   const long long n_big = __ldcg(&a.hdr->n_big);
-  unsigned long long grab = 0;
-  if (lane == 0) grab = atomicAdd(&a.hdr->counter, 1ull);
-  long long t = (long long)__shfl_sync(VMP_FULL, grab, 0);
-  while (t < total_items) {{
-    if (lane == 0) grab = atomicAdd(&a.hdr->counter, 1ull);   // prefetch the next item
+  // striped work queue: stripe s serves items t = VMP_QSTRIPES * i + s; a warp
+  // starts on its own stripe and moves on when it runs dry
+  const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  int stripe = wid % VMP_QSTRIPES, dry = 0;
+  for (;;) {{
+    unsigned long long grab = 0;
+    if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
+    const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
+    if (t >= total_items) {{
+      if (++dry == VMP_QSTRIPES) break;
+      stripe = (stripe + 1) % VMP_QSTRIPES;
+      continue;
+    }}
     long long ci, ri;
     if (t < split) {{
       ci = vmp_find_round(a.off, t, lane);
@@ -409,7 +417,6 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       if (bad && lane == 0)
         atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
     }}
-    t = (long long)__shfl_sync(VMP_FULL, grab, 0);
   }}
   if (a.fused_finalize) {{                  // the last CTA to finish writes the outputs
     __shared__ unsigned vmp_last;

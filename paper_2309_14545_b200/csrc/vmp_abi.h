@@ -32,8 +32,9 @@ typedef struct {
  * where off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest
  * edges (chunks >= HBINS-1) and skip absent chunks. */
 #define VMP_HBINS 1024
+#define VMP_QSTRIPES 16           /* item queue striped over 16 counters (t % 16) */
 typedef struct {
-  unsigned long long counter;     /* work-item queue */
+  unsigned long long counter[VMP_QSTRIPES * 16]; /* stripe s at [16 s]: one 128 B line each */
   unsigned long long total_items; /* written by the scan kernel */
   unsigned int max_chunks;        /* max over edges of ceil(S W / 32), S = ceil(n / W) */
   unsigned int n_big;             /* edges with chunks >= VMP_HBINS - 1 */
