@@ -140,12 +140,12 @@ def _fk_lines(program) -> list[str]:
             arg = a[i]
             si, ci = sin_of.get(arg), cos_of.get(arg)
             if si is not None and ci is not None:
-                lines.append(f"float v{si}, v{ci}; sincosf(v{arg}, &v{si}, &v{ci});")
+                lines.append(f"float v{si}, v{ci}; vmp_sincos(v{arg}, &v{si}, &v{ci});")
                 done.update((si, ci))
             elif k == SIN:
-                lines.append(f"const float v{i} = sinf(v{arg});")
+                lines.append(f"float v{i}, vdummy{i}; vmp_sincos(v{arg}, &v{i}, &vdummy{i});")
             else:
-                lines.append(f"const float v{i} = cosf(v{arg});")
+                lines.append(f"float vdummy{i}, v{i}; vmp_sincos(v{arg}, &vdummy{i}, &v{i});")
         else:
             raise ValueError(f"unknown op kind {k} at {i}")
     return lines
@@ -169,8 +169,8 @@ def _state_function(lay: RobotLayout) -> str:
          "(STOP == 2 && __any_sync(VMP_FULL, !ok && vmp_inr)))")
     emit("  const bool vmp_inr = ok;")
     # all-invalid exits (STOP 1) rarely fire at 20-60 % collision rates: vote every
-    # 4th obstacle; any-invalid exits (STOP 2, motion) pay off at every obstacle
-    emit("  constexpr int VMP_STOP_MASK = STOP == 1 ? 3 : 0;")
+    # 4th obstacle; any-invalid exits (STOP 2, motion) every 2nd
+    emit("  constexpr int VMP_STOP_MASK = STOP == 1 ? 3 : 1;")
     emit("  (void)vmp_inr;")
     # self-collision pairs (compile-time thresholds)
     fine = lay.fine
@@ -405,12 +405,14 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
         s[j] = __ldg(a.starts + ei * a.sld + j);
         g[j] = __ldg(a.goals + ei * a.sld + j);
       }}
-      const long long S = (n + W - 1) / W;
-      const long long p = 32 * ci + lane;
-      const long long j = p / W + 1;
-      const long long k = p - (j - 1) * W;
-      const long long idx = k * S + (a.backward ? (S - j + 1) : j);
-      const bool inr = p < S * W && idx <= n;
+      // 32-bit rake index math (n < 2^31, positions < 2^31 guarded by the plan)
+      const unsigned Wu = (unsigned)a.width;
+      const unsigned S = (unsigned)((n + W - 1) / W);
+      const unsigned p = 32u * (unsigned)ci + lane;
+      const unsigned j = p / Wu + 1;
+      const unsigned k = p - (j - 1) * Wu;
+      const long long idx = (long long)k * S + (a.backward ? (S - j + 1) : j);
+      const bool inr = (long long)p < (long long)S * W && idx <= n;
       const float tt = vmp_rake_param(inr ? idx : 1, n);
       float q[{dofp}];
 #pragma unroll

@@ -47,11 +47,34 @@ REPLACEMENTS = {
 }
 
 _SAVED: dict = {}
+#: calls routed to the B200 path per name (filled when patched with count=True)
+CALLS: dict = {}
 
 
-def patch_vecmp(pkg) -> list[str]:
-    """Rebind the hot-path names in ``pkg`` (the imported vecmp package)."""
+def _counting(name, fn):
+    if isinstance(fn, type):
+        class Counted(fn):
+            def __init__(self, *args, **kwargs):
+                CALLS[name] = CALLS.get(name, 0) + 1
+                super().__init__(*args, **kwargs)
+        Counted.__name__ = Counted.__qualname__ = fn.__name__
+        return Counted
+
+    def wrapper(*args, **kwargs):
+        CALLS[name] = CALLS.get(name, 0) + 1
+        return fn(*args, **kwargs)
+    wrapper.__name__ = fn.__name__
+    wrapper.__doc__ = fn.__doc__
+    return wrapper
+
+
+def patch_vecmp(pkg, count: bool = False) -> list[str]:
+    """Rebind the hot-path names in ``pkg`` (the imported vecmp package).
+
+    With ``count`` every replacement is wrapped to tally its calls in CALLS.
+    """
     done = []
+    table = {k: (_counting(k, v) if count else v) for k, v in REPLACEMENTS.items()}
     for sub, names in TARGETS.items():
         try:
             mod = importlib.import_module(f"{pkg.__name__}.{sub}") if sub else pkg
@@ -60,7 +83,7 @@ def patch_vecmp(pkg) -> list[str]:
         for name in names:
             if hasattr(mod, name):
                 _SAVED.setdefault((mod.__name__, name), getattr(mod, name))
-                setattr(mod, name, REPLACEMENTS[name])
+                setattr(mod, name, table[name])
                 done.append(f"{mod.__name__}.{name}")
     return done
 

@@ -15,7 +15,7 @@ cp -r baseline/_ref/pkg "$WORK/pkg"
 ROOTDIR=$(pwd)
 cd "$WORK/pkg"
 PYTHONPATH="$ROOTDIR:$ROOTDIR/scripts/refsuite:$WORK/pkg/src:$WORK/pkg/tests" \
-  timeout 3000 python -m pytest tests -p vmp_patch_plugin -p no:cacheprovider -q -x ${REF_ARGS:-} \
+  timeout 3000 python -m pytest tests -p vmp_patch_plugin -p no:cacheprovider -q -rf --durations=15 ${REF_ARGS:-} \
   > "$ROOTDIR/gpurun_out/reference_suite.log" 2>&1
 echo "reference suite rc=$?" >> "$ROOTDIR/gpurun_out/reference_suite.log"
 tail -5 "$ROOTDIR/gpurun_out/reference_suite.log"
