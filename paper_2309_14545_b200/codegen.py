@@ -38,7 +38,7 @@ from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
-CODEGEN_VERSION = 3
+CODEGEN_VERSION = 4
 
 
 def f32_literal(value: float) -> str:
@@ -240,21 +240,39 @@ def _state_function(lay: RobotLayout) -> str:
         rs2 = np.float32(np.float32(r) * np.float32(r))
         return f"{box_fn(r)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
 
+    def broadphase(bound: str, radius: str) -> None:
+        # warp-level cull: skip the obstacle unless some lane has some sphere
+        # inside its bounding sphere (exact: the obstacle lies inside the bound)
+        emit("    bool vmp_near = !CULL;")
+        emit("    if (CULL) {")
+        for s in dyn:
+            x, y, z = _xyz(s)
+            emit(f"      vmp_near |= !vmp_clear_sphere({x}, {y}, {z}, S{s.slot}, "
+                 f"{f32_literal(-2.0 * np.float32(s.radius))}, {bound}, {radius});")
+        emit("    }")
+        emit("    if (!CULL || __any_sync(VMP_FULL, vmp_near)) {")
+
     if dyn:
+        # dense mode (STOP 0) runs every test: the honest roofline configuration
+        emit("  constexpr bool CULL = STOP != 0;")
         emit("  const float4 *p = env;")
-        emit("  for (int k = 0; k < ns; ++k, p += 2) {")
+        emit("  for (int k = 0; k < ns; ++k, p += VMP_SPH_F4) {")
         emit("    const float4 r0 = p[0], r1 = p[1];")
         group_tests(sph_test, sph_coarse)
         emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
         emit("  }")
-        emit("  for (int k = 0; k < nc; ++k, p += 3) {")
-        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2];")
+        emit("  for (int k = 0; k < nc; ++k, p += VMP_CAP_F4) {")
+        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3];")
+        broadphase("r3", "r2.w")
         group_tests(cap_test, cap_coarse)
+        emit("    }")
         emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
         emit("  }")
-        emit("  for (int k = 0; k < nb; ++k, p += 4) {")
-        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3];")
+        emit("  for (int k = 0; k < nb; ++k, p += VMP_BOX_F4) {")
+        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3], r4 = p[4];")
+        broadphase("r4", "r3.w")
         group_tests(box_test, box_coarse)
+        emit("    }")
         emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
         emit("  }")
     emit("#undef VMP_STOP_NOW")

@@ -5,12 +5,16 @@
 #define VMP_ABI_H
 
 /* Environment as seen by a kernel: packed float4 records, grouped by kind
- * (spheres: 2 float4, capsules: 3 float4, cuboids: 4 float4 each; layout in
- * DESIGN.md "Data layout in HBM"). */
+ * (spheres: 2 float4, capsules: 4 float4, cuboids: 5 float4 each - the last
+ * record of a capsule / cuboid is its bounding sphere; layout in
+ * csrc/vmp_device.cuh and DESIGN.md "Data layout in HBM"). */
+#define VMP_SPH_F4 2
+#define VMP_CAP_F4 4
+#define VMP_BOX_F4 5
 typedef struct {
   const float4 *rec;   /* device pointer, 16-byte aligned */
   int ns, nc, nb;      /* sphere / capsule / cuboid counts */
-  int n_f4;            /* total float4 records = 2 ns + 3 nc + 4 nb */
+  int n_f4;            /* total float4 records = 2 ns + 4 nc + 5 nb */
 } VmpEnvView;
 
 typedef struct {

@@ -81,8 +81,13 @@ __device__ __forceinline__ const float4 *vmp_env_begin(const VmpEnvView &env, in
 /* ------------------------------------------------------------- narrowphase
  * Records (float4 units), built on the host by vmp_env_create (vmp.cu):
  *   sphere  k: R0 = (-2 o, -( |o|^2 - r^2 )),  R1 = (r, 0, 0, 0)
- *   capsule k: R0 = (a, -p0.a), R1 = (-2 p0, -( |p0|^2 - r^2 )), R2 = (1/|a|^2, |a|^2, r, 0)
- *   cuboid  k: R0..R2 = (row i of R^T, -(R^T c)_i),  R3 = (h, 0)
+ *   capsule k: R0 = (a, -p0.a), R1 = (-2 p0, -( |p0|^2 - r^2 )), R2 = (1/|a|^2, |a|^2, r, Rb),
+ *              R3 = (-2 cb, -( |cb|^2 - Rb^2 ))
+ *   cuboid  k: R0..R2 = (row i of R^T, -(R^T c)_i),  R3 = (h, Rb),
+ *              R4 = (-2 c, -( |c|^2 - Rb^2 ))
+ * (cb, Rb) is the primitive's bounding sphere (capsule: midpoint, half length
+ * + r; cuboid: centre, |h|; both + 1e-5 m), tested like a sphere obstacle for
+ * the warp-level broadphase cull of the generated kernels.
  * For a robot sphere with centre c and radius rs, S = |c|^2 - rs^2 and
  *   |c - o|^2 - (r + rs)^2 = S + r (-2 rs) + (-2 o).c + (|o|^2 - r^2)
  * so the sphere test is 4 FFMA + 1 FSETP.  Hit <=> value <= 0, i.e. boundary
@@ -165,8 +170,8 @@ __device__ __forceinline__ bool vmp_sphere_clear_env(const float4 *rec, int ns, 
   bool ok = true;
   const float4 *p = rec;
   for (int k = 0; k < ns; ++k, p += 2) ok &= vmp_clear_sphere(x, y, z, S, m2rs, p[0], p[1].x);
-  for (int k = 0; k < nc; ++k, p += 3) ok &= vmp_clear_capsule(x, y, z, S, m2rs, p[0], p[1], p[2]);
-  for (int k = 0; k < nb; ++k, p += 4) ok &= vmp_clear_box(x, y, z, rs, rs2, p[0], p[1], p[2], p[3]);
+  for (int k = 0; k < nc; ++k, p += VMP_CAP_F4) ok &= vmp_clear_capsule(x, y, z, S, m2rs, p[0], p[1], p[2]);
+  for (int k = 0; k < nb; ++k, p += VMP_BOX_F4) ok &= vmp_clear_box(x, y, z, rs, rs2, p[0], p[1], p[2], p[3]);
   return ok;
 }
 
