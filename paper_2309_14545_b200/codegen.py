@@ -38,7 +38,8 @@ from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
-CODEGEN_VERSION = 4
+GROUP_SIZE = 3          # dynamic spheres per broadphase group
+CODEGEN_VERSION = 5
 
 
 def f32_literal(value: float) -> str:
@@ -184,6 +185,24 @@ def _state_function(lay: RobotLayout) -> str:
         x, y, z = _xyz(s)
         rs2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
         emit(f"  const float S{s.slot} = vmp_sphere_S({x}, {y}, {z}, {f32_literal(rs2)});")
+    # broadphase groups: consecutive dynamic spheres, bounded per lane by a sphere
+    # centred on the group's middle sphere with the exact (inflated) covering
+    # radius - one bound test per group per obstacle replaces one per sphere
+    groups = [dyn[i:i + GROUP_SIZE] for i in range(0, len(dyn), GROUP_SIZE)]
+    emit("  constexpr bool CULL = STOP != 0;")
+    for gi, grp in enumerate(groups):
+        mid = grp[len(grp) // 2]
+        mx, my, mz = _xyz(mid)
+        emit(f"  float G{gi}R = {f32_literal(mid.radius)};")
+        for s in grp:
+            if s is mid:
+                continue
+            x, y, z = _xyz(s)
+            emit(f"  G{gi}R = fmaxf(G{gi}R, vmp_dist({x}, {y}, {z}, {mx}, {my}, {mz}) + "
+                 f"{f32_literal(s.radius)});")
+        emit(f"  G{gi}R = fmaf(G{gi}R, 1.000002f, 1e-6f);")
+        emit(f"  const float G{gi}S = vmp_sphere_S({mx}, {my}, {mz}, G{gi}R * G{gi}R);")
+        emit(f"  const float G{gi}M = -2.0f * G{gi}R;")
     coarse_links = {link for link in lay.coarse}
     by_link: dict[int, list[FineSphere]] = {}
     for s in dyn:
@@ -241,24 +260,26 @@ def _state_function(lay: RobotLayout) -> str:
         return f"{box_fn(r)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
 
     def broadphase(bound: str, radius: str) -> None:
-        # warp-level cull: skip the obstacle unless some lane has some sphere
-        # inside its bounding sphere (exact: the obstacle lies inside the bound)
+        # warp-level cull: skip the obstacle unless some lane has some group
+        # bound touching the obstacle's bounding sphere (exact: the obstacle lies
+        # inside its bound and every sphere of a group inside the group bound)
         emit("    bool vmp_near = !CULL;")
         emit("    if (CULL) {")
-        for s in dyn:
-            x, y, z = _xyz(s)
-            emit(f"      vmp_near |= !vmp_clear_sphere({x}, {y}, {z}, S{s.slot}, "
-                 f"{f32_literal(-2.0 * np.float32(s.radius))}, {bound}, {radius});")
+        for gi, grp in enumerate(groups):
+            mx, my, mz = _xyz(grp[len(grp) // 2])
+            emit(f"      vmp_near |= !vmp_clear_sphere({mx}, {my}, {mz}, G{gi}S, G{gi}M, "
+                 f"{bound}, {radius});")
         emit("    }")
         emit("    if (!CULL || __any_sync(VMP_FULL, vmp_near)) {")
 
     if dyn:
         # dense mode (STOP 0) runs every test: the honest roofline configuration
-        emit("  constexpr bool CULL = STOP != 0;")
         emit("  const float4 *p = env;")
         emit("  for (int k = 0; k < ns; ++k, p += VMP_SPH_F4) {")
         emit("    const float4 r0 = p[0], r1 = p[1];")
+        broadphase("r0", "r1.x")
         group_tests(sph_test, sph_coarse)
+        emit("    }")
         emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
         emit("  }")
         emit("  for (int k = 0; k < nc; ++k, p += VMP_CAP_F4) {")
@@ -291,12 +312,17 @@ def _const_check(lay: RobotLayout) -> str:
              "  (void)env; (void)ns; (void)nc; (void)nb;",
              "  bool ok = true;"]
     if consts:
-        lines.append("  switch (threadIdx.x) {")
+        # (const sphere, obstacle) pairs spread over the CTA's threads
+        lines.append("  const int nobst = ns + nc + nb;")
+        lines.append(f"  for (int t = threadIdx.x; t < {len(consts)} * nobst; t += blockDim.x) {{")
+        lines.append("    const int k = t % nobst;")
+        lines.append("    switch (t / nobst) {")
         for k, s in enumerate(consts):
             # centre coordinates of a const sphere are CONST ops: exact float32 literals
-            lines.append(f"  case {k}: ok = vmp_sphere_clear_env(env, ns, nc, nb, "
+            lines.append(f"    case {k}: ok &= vmp_sphere_clear_obstacle(env, ns, nc, nb, k, "
                          f"VMP_C{s.slot}X, VMP_C{s.slot}Y, VMP_C{s.slot}Z, {f32_literal(s.radius)}); break;")
-        lines.append("  default: break;")
+        lines.append("    default: break;")
+        lines.append("    }")
         lines.append("  }")
     lines.append("  return ok;")
     lines.append("}")
@@ -397,9 +423,12 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     unsigned long long grab = 0;
     if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
     const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
-    if (t >= total_items) {{
-      if (++dry == VMP_QSTRIPES) break;
-      stripe = (stripe + 1) % VMP_QSTRIPES;
+    if (t >= total_items) {{                // stripe dry: look at all stripes at once
+      const unsigned long long seen = lane < VMP_QSTRIPES ? __ldcg(&a.hdr->counter[16 * lane]) : 0;
+      const unsigned open = __ballot_sync(VMP_FULL, lane < VMP_QSTRIPES &&
+                                          (long long)seen * VMP_QSTRIPES + lane < total_items);
+      if (!open || ++dry > 4 * VMP_QSTRIPES) break;
+      stripe = __ffs(open) - 1;
       continue;
     }}
     long long ci, ri;

@@ -153,11 +153,37 @@ __device__ __forceinline__ bool vmp_clear_box(float x, float y, float z, float r
                    : vmp_clear_box_any(x, y, z, rs2, r0, r1, r2, r3);
 }
 
+/* Euclidean distance with IEEE sqrt (broadphase group radii, rounded up by the caller). */
+__device__ __forceinline__ float vmp_dist(float ax, float ay, float az, float bx, float by,
+                                          float bz) {
+  const float dx = ax - bx, dy = ay - by, dz = az - bz;
+  return __fsqrt_ru(fmaf(dz, dz, fmaf(dy, dy, dx * dx)));
+}
+
 /* Self pair: clear iff d^2 > f32(ra + rb)^2 (reference collision.py:385-394). */
 __device__ __forceinline__ bool vmp_clear_pair(float ax, float ay, float az, float bx, float by,
                                                float bz, float thr) {
   float dx = ax - bx, dy = ay - by, dz = az - bz;
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) > thr;
+}
+
+/* Test one robot sphere against obstacle k (records ordered spheres, capsules, boxes). */
+__device__ __forceinline__ bool vmp_sphere_clear_obstacle(const float4 *rec, int ns, int nc, int nb,
+                                                          int k, float x, float y, float z,
+                                                          float rs) {
+  (void)nb;
+  const float rs2 = rs * rs, m2rs = -2.0f * rs;
+  const float S = vmp_sphere_S(x, y, z, rs2);
+  if (k < ns) {
+    const float4 *p = rec + VMP_SPH_F4 * k;
+    return vmp_clear_sphere(x, y, z, S, m2rs, p[0], p[1].x);
+  }
+  if (k < ns + nc) {
+    const float4 *p = rec + VMP_SPH_F4 * ns + VMP_CAP_F4 * (k - ns);
+    return vmp_clear_capsule(x, y, z, S, m2rs, p[0], p[1], p[2]);
+  }
+  const float4 *p = rec + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc + VMP_BOX_F4 * (k - ns - nc);
+  return vmp_clear_box(x, y, z, rs, rs2, p[0], p[1], p[2], p[3]);
 }
 
 /* Test one robot sphere against every obstacle of env (generic path used by
