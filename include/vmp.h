@@ -104,7 +104,8 @@ int vmp_validate(const vmp_robot *robot, const vmp_env *env, const float *q, int
  *   n_states   : optional, discretization_count per edge (motion.py:25-29)
  *   blocks     : optional, block evaluations the W-wide rake performs
  *   workspace  : >= vmp_motion_workspace_bytes(n_edges) bytes of device
- *                scratch (work queue + per-edge plan); 16-byte aligned
+ *                scratch (work queue + per-edge plan); 16-byte aligned and
+ *                ZERO-FILLED before its first use (calls leave it zeroed)
  * Launches plan -> fused FK+CC rake -> finalize on `stream`. */
 int vmp_validate_motions(const vmp_robot *robot, const vmp_env *env, const float *starts,
                          const float *goals, int64_t n_edges, int64_t sld, double resolution,

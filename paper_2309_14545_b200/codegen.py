@@ -412,6 +412,9 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
   const int lane = threadIdx.x & 31;
   const long long W = a.width;
+  // programmatic dependent launch: everything above (env staging, const check)
+  // overlapped the plan kernel; wait for its results here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const long long total_items = (long long)__ldcg(&a.hdr->total_items);
   const long long split = __ldg(a.off + (VMP_HBINS - 1));
   const long long n_big = __ldcg(&a.hdr->n_big);
@@ -482,6 +485,13 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       __threadfence();
       vmp_motion_outputs(a.n_edges, a.width, a.n_of, a.fail_of, a.bits, a.n_states, a.blocks,
                          0, {BLOCK}, threadIdx.x);
+      // leave the workspace header zeroed for the next call (no memset launch)
+      for (int s = threadIdx.x; s < VMP_QSTRIPES; s += {BLOCK}) a.hdr->counter[16 * s] = 0;
+      if (threadIdx.x == 0) {{
+        a.hdr->max_chunks = 0;
+        a.hdr->done_ctas = 0;
+        a.hdr->plan_done = 0;
+      }}
     }}
   }}
 }}
