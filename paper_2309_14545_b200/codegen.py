@@ -415,9 +415,15 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // programmatic dependent launch: everything above (env staging, const check)
   // overlapped the plan kernel; wait for its results here
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // plan data was written while this grid was already running: read it through
+  // L2 (ld.global.cg), never the non-coherent path; round offsets go to smem
   const long long total_items = (long long)__ldcg(&a.hdr->total_items);
-  const long long split = __ldg(a.off + (VMP_HBINS - 1));
+  const long long split = __ldcg(a.off + (VMP_HBINS - 1));
   const long long n_big = __ldcg(&a.hdr->n_big);
+  __shared__ long long vmp_off[VMP_HBINS];
+  const int n_off = (int)min(__ldcg(&a.hdr->max_chunks) + 1u, (unsigned)VMP_HBINS);
+  for (int i = threadIdx.x; i < n_off; i += blockDim.x) vmp_off[i] = __ldcg(a.off + i);
+  __syncthreads();
   // striped work queue: stripe s serves items t = VMP_QSTRIPES * i + s; a warp
   // starts on its own stripe and moves on when it runs dry
   const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
@@ -436,18 +442,18 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     }}
     long long ci, ri;
     if (t < split) {{
-      ci = vmp_find_round(a.off, t, lane);
-      ri = t - __ldg(a.off + ci);
+      ci = vmp_find_round(vmp_off, n_off, t, lane);
+      ri = t - vmp_off[ci];
     }} else {{                              // rounds beyond the histogram (very long edges)
       const long long u = t - split;
       ci = (VMP_HBINS - 1) + u / n_big;
       ri = u - (ci - (VMP_HBINS - 1)) * n_big;
     }}
-    const long long ei = __ldg(a.order + ri);
+    const long long ei = __ldcg(a.order + ri);
     const long long first_iter = (32 * ci) / W + 1;
-    const int chunks = __ldg(a.chunks_of + ei);
+    const int chunks = __ldcg(a.chunks_of + ei);
     const int failed = __ldcg(a.fail_of + ei);
-    const long long n = __ldg(a.n_of + ei);
+    const long long n = __ldcg(a.n_of + ei);
     if (ci < chunks && failed > (int)first_iter) {{   // else: absent, or cannot lower the count
       float s[{dofp}], g[{dofp}];
 #pragma unroll
@@ -475,6 +481,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   }}
   if (a.fused_finalize) {{                  // the last CTA to finish writes the outputs
     __shared__ unsigned vmp_last;
+    __threadfence();                        // publish this warp's fail_of updates device-wide
     __syncthreads();
     if (threadIdx.x == 0) {{
       __threadfence();

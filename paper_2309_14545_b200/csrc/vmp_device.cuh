@@ -271,7 +271,7 @@ __device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width,
     const unsigned m = __ballot_sync(VMP_FULL, ok);
     if (inr) {
       if ((tid & 31) == 0) bits[e >> 5] = m;
-      const long long n = n_of[e];
+      const long long n = __ldcg(n_of + e);
       if (n_states) n_states[e] = (int)n;
       if (blocks) blocks[e] = ok ? (int)((n + width - 1) / width) : fail;
     }
@@ -280,11 +280,12 @@ __device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width,
 
 /* Round c of the motion work list holding item t: the largest c with
  * off[c] <= t, found 32 rounds per step with one load per lane + ballot. */
-__device__ __forceinline__ int vmp_find_round(const long long *off, long long t, int lane) {
+__device__ __forceinline__ int vmp_find_round(const long long *off, int n_off, long long t,
+                                              int lane) {
   int base = 0;
   for (;;) {
     const int c = base + lane;
-    const bool le = c < VMP_HBINS && __ldg(off + c) <= t;
+    const bool le = c < n_off && off[c] <= t;
     const unsigned m = __ballot_sync(VMP_FULL, le);
     if (m != VMP_FULL || base + 32 >= VMP_HBINS) return base + 31 - __clz(m);
     base += 32;

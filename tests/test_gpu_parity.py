@@ -279,3 +279,26 @@ def test_motion_errors(cuda):
     from paper_2309_14545_b200 import Environment
     free = ValidationContext(rob.program, rob.model, rob.pairs, Environment())
     assert M.raked_motion_check(q, q, free, 0.05) == (True, 1)
+
+
+def test_motion_repeated_calls_consistent(cuda):
+    """Back-to-back launches (fresh and reused self-cleaning workspaces, PDL
+    overlap of plan and rake kernels) give identical results every time."""
+    fx = golden_io.load("motion")
+    key = "arm7_0"
+    rob = load_robot("arm7")
+    env = golden_io.env_from(fx, f"env_{key}")
+    s, g, res = fx[f"starts_{key}"], fx[f"goals_{key}"], float(fx[f"res_{key}"])
+    ws = runtime.motion_workspace(len(s))
+    for rep in range(12):
+        width = (8, 32, 1)[rep % 3]
+        ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=width)
+        b, n, blk = M.validate_motions(ctx, s, g, res, width=width, counts=True,
+                                       workspace=ws if rep % 2 else None)
+        assert runtime.unpack_bits(b.cpu().numpy(), len(s)).tolist() == \
+            fx[f"verdict_{key}_w{width}_b0"].tolist()
+        assert blk.cpu().numpy().tolist() == fx[f"blocks_{key}_w{width}_b0"].tolist()
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=8)
+    for i in range(len(s)):
+        assert M.raked_motion_check(s[i], g[i], ctx, res) == (
+            bool(fx[f"verdict_{key}_w8_b0"][i]), int(fx[f"blocks_{key}_w8_b0"][i]))
