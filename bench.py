@@ -307,56 +307,69 @@ def fkcc_summary(ctx_flush, peak: float) -> dict:
 
 # ------------------------------------------------------- CPU reference arm
 
-def _cpu_worker(payload):
+_CPU = {}
+
+
+def _cpu_init() -> None:
+    """Per-process state of the CPU arm: oracle port, robot program, workload."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import vecmp_oracle as O
     from paper_2309_14545_b200 import load_robot, workloads
-    idx = payload
     mw = workloads.config2()
     rob = load_robot(mw.robot)
-    ob = O.Obstacles(mw.env.primitives)
-    t0 = time.perf_counter()
-    verdicts = [O.rake_check(rob.program, rob.pairs, ob, mw.starts[i], mw.goals[i], mw.resolution, 8)[0]
-                for i in idx]
-    return time.perf_counter() - t0, verdicts
+    _CPU.update(O=O, mw=mw, rob=rob, ob=O.Obstacles(mw.env.primitives))
+
+
+def _cpu_worker(idx):
+    if not _CPU:
+        _cpu_init()
+    O, mw, rob, ob = _CPU["O"], _CPU["mw"], _CPU["rob"], _CPU["ob"]
+    return [O.rake_check(rob.program, rob.pairs, ob, mw.starts[i], mw.goals[i], mw.resolution, 8)[0]
+            for i in idx]
+
+
+def _sample(n_edges: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(4096, size=min(n_edges, 4096), replace=False))
 
 
 def cpu_baseline_motion(mw, rob, processes: int, n_edges: int) -> dict:
-    """Oracle port (bit-exact restatement of the reference) on host cores:
-    ValidationContext(width=8)-style rake per edge, as the reference runs it."""
-    rng = np.random.default_rng(123)
-    idx = np.sort(rng.choice(len(mw.starts), size=min(n_edges, len(mw.starts)), replace=False))
-    chunks = [idx[i::processes] for i in range(processes)]
+    """Oracle port (bit-exact restatement of the reference) on one host core:
+    the ValidationContext(width=8) rake per edge, as the reference runs it."""
+    _cpu_init()
+    idx = _sample(n_edges, 123)
+    _cpu_worker(idx[:8])                                  # warm caches
     t0 = time.perf_counter()
-    if processes == 1:
-        results = [_cpu_worker(chunks[0])]
-    else:
-        import multiprocessing as mp
-        with mp.get_context("fork").Pool(processes) as pool:
-            results = pool.map(_cpu_worker, chunks)
+    _cpu_worker(idx)
     wall = time.perf_counter() - t0
-    return {"value": round(len(idx) / wall, 2), "unit": "edges/s", "cores": processes,
-            "kind": "port",
+    return {"value": round(len(idx) / wall, 2), "unit": "edges/s", "cores": 1, "kind": "port",
             "sample": f"{len(idx)} seeded-random edges of the 4,096 (W=8 rake, numpy "
-                      f"{np.__version__}, {processes} process(es), {wall:.1f} s wall)"}
+                      f"{np.__version__}, 1 process, {wall:.1f} s wall)"}
 
 
 def run_reference(args, rank: int, world: int) -> dict | None:
     if rank != 0:
         return None
+    import multiprocessing as mp
+
     from paper_2309_14545_b200 import load_robot, workloads
     mw = workloads.config2()
     rob = load_robot(mw.robot)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    per_step = max(cores * 4, 64)
-    for _ in range(min(args.warmup, 1)):
-        cpu_baseline_motion(mw, rob, cores, min(per_step, 64))
-    vals = []
-    t_total = 0.0
-    for k in range(args.steps):
-        r = cpu_baseline_motion(mw, rob, cores, per_step)
-        vals.append(r["value"])
-        t_total += per_step / r["value"]
+    per_step = max(cores * 8, 64)
+    pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init)
+    try:
+        for w in range(args.warmup):
+            pool.map(_cpu_worker, np.array_split(_sample(cores, 7 + w), cores))
+        t_total = 0.0
+        for k in range(args.steps):
+            idx = _sample(per_step, 1000 + k)
+            t0 = time.perf_counter()
+            pool.map(_cpu_worker, np.array_split(idx, cores))
+            t_total += time.perf_counter() - t0
+    finally:
+        pool.close()
+        pool.join()
     value = args.steps * per_step / t_total
     return {
         "impl": "reference",
