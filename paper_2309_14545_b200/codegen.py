@@ -39,7 +39,7 @@ from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
 CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
-CODEGEN_VERSION = 5
+CODEGEN_VERSION = 6
 
 
 def f32_literal(value: float) -> str:
@@ -173,13 +173,7 @@ def _state_function(lay: RobotLayout) -> str:
     # 4th obstacle; any-invalid exits (STOP 2, motion) every 2nd
     emit("  constexpr int VMP_STOP_MASK = STOP == 1 ? 3 : 1;")
     emit("  (void)vmp_inr;")
-    # self-collision pairs (compile-time thresholds)
     fine = lay.fine
-    for sa, sb, thr in lay.pairs:
-        ax, ay, az = _xyz(fine[sa])
-        bx, by, bz = _xyz(fine[sb])
-        emit(f"  ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
-    emit("  if (VMP_STOP_NOW) return ok;")
     # per-sphere constants
     for s in dyn:
         x, y, z = _xyz(s)
@@ -203,6 +197,40 @@ def _state_function(lay: RobotLayout) -> str:
         emit(f"  G{gi}R = fmaf(G{gi}R, 1.000002f, 1e-6f);")
         emit(f"  const float G{gi}S = vmp_sphere_S({mx}, {my}, {mz}, G{gi}R * G{gi}R);")
         emit(f"  const float G{gi}M = -2.0f * G{gi}R;")
+    # self-collision pairs (compile-time thresholds), bucketed by group pair;
+    # constant spheres are singleton groups with their exact centre and radius.
+    # A bucket is skipped when no lane has its two group bounds overlapping.
+    group_of: dict[int, tuple] = {}
+    for gi, grp in enumerate(groups):
+        mxyz = _xyz(grp[len(grp) // 2])
+        for s in grp:
+            group_of[s.slot] = (f"g{gi:03d}", mxyz, f"G{gi}R")
+    for s in lay.const_spheres:
+        group_of[s.slot] = (f"c{s.slot:03d}", _xyz(s), f32_literal(s.radius))
+    buckets: dict[tuple, list] = {}
+    for sa, sb, thr in lay.pairs:
+        ka, kb = group_of[sa][0], group_of[sb][0]
+        key = (ka, kb) if ka <= kb else (kb, ka)
+        buckets.setdefault(key, []).append((sa, sb, thr))
+    by_name = {v[0]: v for v in group_of.values()}
+    for (ka, kb), items in buckets.items():
+        tests = []
+        for sa, sb, thr in items:
+            ax, ay, az = _xyz(fine[sa])
+            bx, by, bz = _xyz(fine[sb])
+            tests.append(f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, "
+                         f"{f32_literal(thr)});")
+        if ka == kb or (ka[0] == "c" and kb[0] == "c"):
+            for t in tests:
+                emit("  " + t)
+            continue
+        (_, (ax, ay, az), ra), (_, (bx, by, bz), rb) = by_name[ka], by_name[kb]
+        emit(f"  if (!CULL || __any_sync(VMP_FULL, !vmp_clear_pair({ax}, {ay}, {az}, {bx}, {by}, "
+             f"{bz}, ({ra} + {rb}) * ({ra} + {rb})))) {{")
+        for t in tests:
+            emit("    " + t)
+        emit("  }")
+    emit("  if (VMP_STOP_NOW) return ok;")
     coarse_links = {link for link in lay.coarse}
     by_link: dict[int, list[FineSphere]] = {}
     for s in dyn:
