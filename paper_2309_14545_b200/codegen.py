@@ -174,6 +174,16 @@ def _state_function(lay: RobotLayout) -> str:
     emit("  constexpr int VMP_STOP_MASK = STOP == 1 ? 3 : 1;")
     emit("  (void)vmp_inr;")
     fine = lay.fine
+    # batch validation (random configurations in a warp): plain self pairs first,
+    # before the broadphase state is live; the motion rake (coherent lanes along
+    # an edge, STOP 2) culls whole pair buckets with the group bounds below
+    emit("  constexpr bool CULL_SELF = STOP == 2;")
+    emit("  if constexpr (!CULL_SELF) {")
+    for sa, sb, thr in lay.pairs:
+        ax, ay, az = _xyz(fine[sa])
+        bx, by, bz = _xyz(fine[sb])
+        emit(f"    ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
+    emit("  }")
     # per-sphere constants
     for s in dyn:
         x, y, z = _xyz(s)
@@ -213,23 +223,25 @@ def _state_function(lay: RobotLayout) -> str:
         key = (ka, kb) if ka <= kb else (kb, ka)
         buckets.setdefault(key, []).append((sa, sb, thr))
     by_name = {v[0]: v for v in group_of.values()}
+    emit("  if constexpr (CULL_SELF) {")
     for (ka, kb), items in buckets.items():
         tests = []
         for sa, sb, thr in items:
             ax, ay, az = _xyz(fine[sa])
             bx, by, bz = _xyz(fine[sb])
             tests.append(f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, "
-                         f"{f32_literal(thr)});")
+                         f"{f32_literal(thr)}); ")
         if ka == kb or (ka[0] == "c" and kb[0] == "c"):
             for t in tests:
                 emit("  " + t)
             continue
         (_, (ax, ay, az), ra), (_, (bx, by, bz), rb) = by_name[ka], by_name[kb]
-        emit(f"  if (!CULL || __any_sync(VMP_FULL, !vmp_clear_pair({ax}, {ay}, {az}, {bx}, {by}, "
+        emit(f"  if (__any_sync(VMP_FULL, !vmp_clear_pair({ax}, {ay}, {az}, {bx}, {by}, "
              f"{bz}, ({ra} + {rb}) * ({ra} + {rb})))) {{")
         for t in tests:
             emit("    " + t)
         emit("  }")
+    emit("  }")
     emit("  if (VMP_STOP_NOW) return ok;")
     coarse_links = {link for link in lay.coarse}
     by_link: dict[int, list[FineSphere]] = {}
