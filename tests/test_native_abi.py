@@ -55,7 +55,8 @@ def test_generated_source_structure():
         assert k in src
     lay = codegen.derive_layout(rob.program, rob.pairs)
     assert len(lay.fine) == 11 and len(lay.pairs) == 42 and len(lay.const_spheres) == 2
-    assert src.count("ok &= vmp_clear_pair(") == 42    # every listed sphere pair, once
+    # every listed sphere pair twice: plain (batch) and group-culled (motion rake)
+    assert src.count("ok &= vmp_clear_pair(") == 2 * 42
     # bundled cubins were prebuilt by build()
     assert runtime.prepare(rob.program, rob.pairs).exists()
 
