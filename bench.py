@@ -123,6 +123,14 @@ def rake_state_counts(n: np.ndarray, blocks: np.ndarray, valid: np.ndarray, widt
     return np.where(valid, full, part)
 
 
+def _traffic(kernel: str):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu capture, or None."""
+    path = ROOT / "profiles" / "traffic.json"
+    if not path.exists():
+        return None
+    return json.loads(path.read_text()).get(kernel)
+
+
 # ----------------------------------------------------------- our GPU arm
 
 def run_ours(args, rank: int, world: int) -> dict | None:
@@ -245,7 +253,8 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                    "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
                    "parallelism": f"dp{world} (independent edges per rank)"},
         "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
-                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                     "traffic": _traffic("vmp_motion_p1_s2_g1"),
                      "kernel": "vmp_motion_p1_s2_g1",
                      "algorithmic_flop_per_state": f_state,
                      "states_counted_per_launch": int(states.sum()),
