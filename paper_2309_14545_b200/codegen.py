@@ -468,10 +468,16 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // starts on its own stripe and moves on when it runs dry
   const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   int stripe = wid % VMP_QSTRIPES, dry = 0;
+  // the next item's atomic is issued before the current chunk is evaluated
+  // (hides the L2 atomic round trip) unless the queue is nearly drained, where
+  // holding a reserved item would lengthen the tail
+  const long long guard = (long long)gridDim.x * (blockDim.x >> 5);
+  unsigned long long grab = 0;
+  bool have = false;
   for (;;) {{
-    unsigned long long grab = 0;
-    if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
+    if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
     const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
+    have = false;
     if (t >= total_items) {{                // stripe dry: look at all stripes at once
       const unsigned long long seen = lane < VMP_QSTRIPES ? __ldcg(&a.hdr->counter[16 * lane]) : 0;
       const unsigned open = __ballot_sync(VMP_FULL, lane < VMP_QSTRIPES &&
@@ -479,6 +485,10 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       if (!open || ++dry > 4 * VMP_QSTRIPES) break;
       stripe = __ffs(open) - 1;
       continue;
+    }}
+    if (t + guard < total_items) {{
+      if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
+      have = true;
     }}
     long long ci, ri;
     if (t < split) {{
@@ -489,11 +499,12 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       ci = (VMP_HBINS - 1) + u / n_big;
       ri = u - (ci - (VMP_HBINS - 1)) * n_big;
     }}
-    const long long ei = __ldcg(a.order + ri);
+    const int4 rank = __ldcg(a.order + ri);                 // (edge, n, chunks, 0)
+    const long long ei = rank.x;
     const long long first_iter = (32 * ci) / W + 1;
-    const int chunks = __ldcg(a.chunks_of + ei);
+    const int chunks = rank.z;
     const int failed = __ldcg(a.fail_of + ei);
-    const long long n = __ldcg(a.n_of + ei);
+    const long long n = rank.y;
     if (ci < chunks && failed > (int)first_iter) {{   // else: absent, or cannot lower the count
       float s[{dofp}], g[{dofp}];
 #pragma unroll

@@ -31,7 +31,8 @@ typedef struct {
  *   VmpMotionHeader
  *   unsigned hist[VMP_HBINS], fill[VMP_HBINS]   chunk-count histogram / scatter cursors
  *   long long off[VMP_HBINS]                    first work item of chunk round c
- *   int n[E], chunks[E], fail[E], order[E]      per-edge plan, order = edges by chunks desc
+ *   int n[E], chunks[E], fail[E]                per-edge plan
+ *   int4 order[E]                               (edge, n, chunks, 0) by chunk count desc
  * Work item t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c,
  * where off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest
  * edges (chunks >= HBINS-1) and skip absent chunks. */
@@ -44,6 +45,7 @@ typedef struct {
   unsigned int n_big;             /* edges with chunks >= VMP_HBINS - 1 */
   unsigned int done_ctas;         /* CTAs of the rake kernel that finished */
   unsigned int plan_done;         /* CTAs of the fused plan kernel that finished */
+  unsigned int pad_[2];           /* keep the arrays behind 16-byte aligned */
 } VmpMotionHeader;
 
 typedef struct {
@@ -58,7 +60,7 @@ typedef struct {
   const int *n_of;      /* discretisation count per edge (plan kernel) */
   const int *chunks_of; /* 32-position chunks per edge (plan kernel) */
   int *fail_of;         /* first failing rake iteration, INT_MAX while none */
-  const int *order;     /* edges sorted by chunk count, descending */
+  const int4 *order;    /* rank records (edge, n, chunks, 0), chunk count descending */
   unsigned int *bits;   /* outputs, written by the last CTA when fused_finalize */
   int *n_states;
   int *blocks;
