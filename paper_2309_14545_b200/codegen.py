@@ -39,7 +39,7 @@ from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
 CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
-CODEGEN_VERSION = 6
+CODEGEN_VERSION = 7
 
 
 def f32_literal(value: float) -> str:
@@ -248,19 +248,17 @@ def _state_function(lay: RobotLayout) -> str:
     for s in dyn:
         by_link.setdefault(s.link, []).append(s)
 
-    def group_tests(test_fn, coarse_fn) -> None:
-        emitted_links = []
+    def group_tests(test_fn, coarse_fn, ind: str = "    ") -> None:
         for link, spheres in by_link.items():
             tests = [test_fn(s) for s in spheres]
             if link in coarse_links and len(spheres) >= 2:
-                emit("    if (!PRUNE || __any_sync(VMP_FULL, !" + coarse_fn(link) + ")) {")
+                emit(ind + "if (!PRUNE || __any_sync(VMP_FULL, !" + coarse_fn(link) + ")) {")
                 for t in tests:
-                    emit("      ok &= " + t + ";")
-                emit("    }")
+                    emit(ind + "  ok &= " + t + ";")
+                emit(ind + "}")
             else:
                 for t in tests:
-                    emit("    ok &= " + t + ";")
-            emitted_links.append(link)
+                    emit(ind + "ok &= " + t + ";")
 
     def coarse_xyz(link):
         r, xyz = lay.coarse[link]
@@ -299,43 +297,52 @@ def _state_function(lay: RobotLayout) -> str:
         rs2 = np.float32(np.float32(r) * np.float32(r))
         return f"{box_fn(r)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
 
-    def broadphase(bound: str, radius: str) -> None:
-        # warp-level cull: skip the obstacle unless some lane has some group
-        # bound touching the obstacle's bounding sphere (exact: the obstacle lies
-        # inside its bound and every sphere of a group inside the group bound)
-        emit("    bool vmp_near = !CULL;")
-        emit("    if (CULL) {")
+    def kind_loop(count: str, f4: str, loads: str, bound: str, radius: str, test_fn, coarse_fn):
+        # dense mode (STOP 0): every obstacle, every test - the honest roofline run
+        emit("  if constexpr (!CULL) {")
+        emit(f"    for (int k = 0; k < {count}; ++k, p += {f4}) {{")
+        emit(f"      const float4 {loads};")
+        group_tests(test_fn, coarse_fn, "      ")
+        emit("    }")
+        emit("  } else {")
+        # product mode, two passes per 32 obstacles: (1) branch-free bound tests
+        # of every group against every obstacle bound into a per-lane bit mask,
+        # (2) one warp OR, then full tests only for obstacles near some lane.
+        # Exact: an obstacle lies inside its bound, every sphere inside its group bound.
+        emit(f"    for (int k0 = 0; k0 < {count}; k0 += 32, p += 32 * {f4}) {{")
+        emit(f"      const int kn = min(32, {count} - k0);")
+        emit("      unsigned near = 0;")
+        emit("      for (int j = 0; j < kn; ++j) {")
+        emit(f"        const float4 *pp = p + j * {f4};")
+        emit(f"        const float4 bnd = pp[{bound}];")
+        emit(f"        const float brad = {radius};")
+        emit("        bool nr = false;")
         for gi, grp in enumerate(groups):
             mx, my, mz = _xyz(grp[len(grp) // 2])
-            emit(f"      vmp_near |= !vmp_clear_sphere({mx}, {my}, {mz}, G{gi}S, G{gi}M, "
-                 f"{bound}, {radius});")
+            emit(f"        nr |= !vmp_clear_sphere({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad);")
+        emit("        near |= (unsigned)nr << j;")
+        emit("      }")
+        emit("      unsigned todo = __reduce_or_sync(VMP_FULL, near);")
+        emit("      while (todo) {")
+        emit("        const int j = __ffs(todo) - 1;")
+        emit("        todo &= todo - 1;")
+        emit(f"        const float4 *pp = p + j * {f4};")
+        emit(f"        const float4 {loads.replace('p[', 'pp[')};")
+        group_tests(test_fn, coarse_fn, "        ")
+        emit("        if (VMP_STOP_NOW) return ok;")
+        emit("      }")
         emit("    }")
-        emit("    if (!CULL || __any_sync(VMP_FULL, vmp_near)) {")
+        emit("  }")
 
     if dyn:
-        # dense mode (STOP 0) runs every test: the honest roofline configuration
         emit("  const float4 *p = env;")
-        emit("  for (int k = 0; k < ns; ++k, p += VMP_SPH_F4) {")
-        emit("    const float4 r0 = p[0], r1 = p[1];")
-        broadphase("r0", "r1.x")
-        group_tests(sph_test, sph_coarse)
-        emit("    }")
-        emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
-        emit("  }")
-        emit("  for (int k = 0; k < nc; ++k, p += VMP_CAP_F4) {")
-        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3];")
-        broadphase("r3", "r2.w")
-        group_tests(cap_test, cap_coarse)
-        emit("    }")
-        emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
-        emit("  }")
-        emit("  for (int k = 0; k < nb; ++k, p += VMP_BOX_F4) {")
-        emit("    const float4 r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3], r4 = p[4];")
-        broadphase("r4", "r3.w")
-        group_tests(box_test, box_coarse)
-        emit("    }")
-        emit("    if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
-        emit("  }")
+        kind_loop("ns", "VMP_SPH_F4", "r0 = p[0], r1 = p[1]", "0", "pp[1].x", sph_test, sph_coarse)
+        emit("  p = env + VMP_SPH_F4 * ns;")
+        kind_loop("nc", "VMP_CAP_F4", "r0 = p[0], r1 = p[1], r2 = p[2]", "3", "pp[2].w",
+                  cap_test, cap_coarse)
+        emit("  p = env + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc;")
+        kind_loop("nb", "VMP_BOX_F4", "r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3]", "4", "pp[3].w",
+                  box_test, box_coarse)
     emit("#undef VMP_STOP_NOW")
     emit("  return ok;")
     emit("}")
