@@ -304,8 +304,22 @@ def _state_function(lay: RobotLayout) -> str:
         emit(f"      const float4 {loads};")
         group_tests(test_fn, coarse_fn, "      ")
         emit("    }")
+        emit("  } else if constexpr (STOP == 1) {")
+        # batch validation: one pass, a warp vote per obstacle on the group bounds
+        emit(f"    for (int k = 0; k < {count}; ++k, p += {f4}) {{")
+        emit(f"      const float4 {loads};")
+        emit("      bool nr = false;")
+        for gi, grp in enumerate(groups):
+            mx, my, mz = _xyz(grp[len(grp) // 2])
+            emit(f"      nr |= !vmp_clear_sphere({mx}, {my}, {mz}, G{gi}S, G{gi}M, p[{bound}], "
+                 f"{radius.replace('pp[', 'p[')});")
+        emit("      if (__any_sync(VMP_FULL, nr)) {")
+        group_tests(test_fn, coarse_fn, "        ")
+        emit("      }")
+        emit("      if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
+        emit("    }")
         emit("  } else {")
-        # product mode, two passes per 32 obstacles: (1) branch-free bound tests
+        # motion rake, two passes per 32 obstacles: (1) branch-free bound tests
         # of every group against every obstacle bound into a per-lane bit mask,
         # (2) one warp OR, then full tests only for obstacles near some lane.
         # Exact: an obstacle lies inside its bound, every sphere inside its group bound.
