@@ -127,6 +127,12 @@ int vmp_discretize(const float *starts, const float *goals, int64_t n_edges, int
 int vmp_sphere_hits(const vmp_env *env, const float *xyz, int64_t n, int64_t ld, float radius,
                     uint8_t *hits, void *stream);
 
+/* Lane-wise self-pair test of two sphere-centre streams a, b (3 x ld each):
+ * clear[i] = |a_i - b_i|^2 > thr, thr = f32(ra + rb)^2 (reference
+ * collision.py:385-394).  Backs the BlockValidator sink. */
+int vmp_pair_clear(const float *a, const float *b, int64_t n, int64_t ld, float thr,
+                   uint8_t *clear, void *stream);
+
 /* Select the CUDA device used by subsequent vmp calls on this thread (robots
  * and environments remember the device they were created on). */
 int vmp_set_device(int32_t device);

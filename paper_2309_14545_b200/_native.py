@@ -39,7 +39,7 @@ EXPORTS = (
     "vmp_version", "vmp_last_error", "vmp_compile", "vmp_robot_load", "vmp_robot_destroy",
     "vmp_env_create", "vmp_env_destroy", "vmp_env_bytes", "vmp_fk_rows", "vmp_fk_spheres",
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
-    "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes",
+    "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
 )
 
 
@@ -103,6 +103,7 @@ def lib() -> ctypes.CDLL:
         "vmp_motion_workspace_bytes": ([c_i64], c_i64),
         "vmp_discretize": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, vp, vp], ctypes.c_int),
         "vmp_sphere_hits": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),
+        "vmp_pair_clear": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),
         "vmp_set_device": ([c_i32], ctypes.c_int),
         "vmp_device_info": ([ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)], ctypes.c_int),
     }

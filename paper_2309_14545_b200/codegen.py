@@ -397,7 +397,7 @@ def _kernels(lay: RobotLayout, program) -> str:
     centre_rows = []
     for m, marker in enumerate(program.checks):
         for c, v in enumerate(marker.xyz):
-            centre_rows.append(f"    o[{3 * m + c} * a.ldo] = v{int(v)};")
+            centre_rows.append(f"    __stcs(o + {3 * m + c} * a.ldo, v{int(v)});")
     centre_rows = "\n".join(centre_rows)
     src = f"""
 extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_rows(VmpFkArgs a) {{
@@ -413,11 +413,25 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_rows(VmpFkArgs a) {
 }}
 
 extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_spheres(VmpFkArgs a) {{
-  for (long long i = blockIdx.x * (long long){BLOCK} + threadIdx.x; i < a.n;
-       i += (long long)gridDim.x * {BLOCK}) {{
+  // HBM-bound: the next configuration's joints are prefetched while this one's
+  // centres are computed; centres leave with streaming (evict-first) stores
+  const long long stride = (long long)gridDim.x * {BLOCK};
+  long long i = blockIdx.x * (long long){BLOCK} + threadIdx.x;
+  float qn[{dofp}];
+  if (i < a.n) {{
     const long long ii = i;
-    float q[{dofp}];
+    float *q = qn;
 {ld_q}
+  }}
+  for (; i < a.n; i += stride) {{
+    float q[{dofp}];
+#pragma unroll
+    for (int j = 0; j < {dofp}; ++j) q[j] = qn[j];
+    if (i + stride < a.n) {{
+      const long long ii = i + stride;
+      float *q = qn;
+{ld_q}
+    }}
     VMP_FK_BODY
     float *o = a.out + i;
 {centre_rows}

@@ -185,6 +185,33 @@ def test_padding_permutation_and_edges(cuda):
     assert engulf.validate_configs(np.zeros((7, 0), np.float32)).size == 0
 
 
+def test_block_validator_sink_matches_fused_path(cuda):
+    """The GPU-backed BlockValidator sink (reference collision.py:293-408) driven
+    by evaluate_program gives the fused kernel's verdicts, and aborts early."""
+    from paper_2309_14545_b200 import BlockValidator, Environment, SphereObstacle
+    fx = golden_io.load("blocks")
+    rob = load_robot("arm7")
+    env = golden_io.env_from(fx, "env_arm7_4")
+    q = fx["q_arm7"][:, :64]
+    fused = validate_block(rob.program, rob.model, rob.pairs, env, ConfigBlock(7, 64, q, 64))
+    for reject_all in (False, True):
+        sink = BlockValidator(env.packed(), rob.pairs, width=64, reject_all=reject_all)
+        evaluate_program(rob.program, ConfigBlock(7, 64, np.ascontiguousarray(q), 64), sink)
+        expect = np.zeros(64, bool) if reject_all and not fused.all() else fused
+        assert np.array_equal(sink.result(), expect)
+    engulf = Environment([SphereObstacle(np.zeros(3), 3.0)])
+    calls = []
+
+    def counting(m, x, y, z, inner=BlockValidator(engulf.packed(), rob.pairs, width=8)):
+        calls.append(m)
+        counting.inner = inner
+        return inner(m, x, y, z)
+
+    evaluate_program(rob.program, soa_from_aos([q[:, 0].copy()], width=8), counting)
+    assert not counting.inner.result().any()
+    assert len(calls) < len(rob.program.checks)
+
+
 # ---------------------------------------------------------- narrowphase
 
 def test_single_obstacle_lane_wrappers_vs_reference(cuda):
