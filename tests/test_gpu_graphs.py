@@ -1,0 +1,49 @@
+"""CUDA-graph fixed-size entry points give the same verdicts as the eager path."""
+
+import numpy as np
+import pytest
+
+import vecmp_oracle as O
+from paper_2309_14545_b200 import ValidationContext, load_robot, runtime, workloads
+from paper_2309_14545_b200 import motion as M
+
+pytestmark = pytest.mark.gpu
+
+
+def test_motion_validator_graph_matches_eager_and_oracle(cuda):
+    torch = cuda
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    eager = runtime.unpack_bits(
+        M.validate_motions(ctx, mw.starts, mw.goals, mw.resolution).cpu().numpy(), len(mw.starts))
+    mv = M.MotionValidator(ctx, len(mw.starts), mw.resolution)
+    hs = torch.from_numpy(mw.starts).pin_memory()
+    hg = torch.from_numpy(mw.goals).pin_memory()
+    for _ in range(5):                       # replays with fresh host inputs each time
+        mv(hs, hg)
+        assert mv.verdicts().tolist() == eager.tolist()
+    # a different batch through the same graph
+    rng = np.random.default_rng(9)
+    idx = rng.permutation(len(mw.starts))
+    mv(mw.starts[idx], mw.goals[idx])
+    assert mv.verdicts().tolist() == eager[idx].tolist()
+    ob = O.Obstacles(mw.env.primitives)
+    for i in range(0, len(mw.starts), 97):
+        _, v = O.edge_all_states(rob.program, rob.pairs, ob, mw.starts[i], mw.goals[i], mw.resolution)
+        assert bool(v.all()) == bool(eager[i])
+
+
+@pytest.mark.parametrize("early", [True, False])
+def test_config_validator_graph(cuda, early):
+    wl = workloads.config3(1 << 16)
+    rob = load_robot(wl.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    n = wl.q.shape[1]
+    cv = ctx.batch_validator(n, early_exit=early)
+    cv(wl.q)
+    got = runtime.unpack_bits(cv().cpu().numpy(), n)
+    assert np.array_equal(got, ctx.validate_configs(wl.q))
+    q2 = workloads.uniform_configs(rob.limits, n, 77)
+    cv(q2)
+    assert np.array_equal(runtime.unpack_bits(cv().cpu().numpy(), n), ctx.validate_configs(q2))
