@@ -34,7 +34,9 @@ extern "C" {
 
 /* vmp_validate flags (reference collision.py:411-430 keyword arguments) */
 #define VMP_PRUNE 1u         /* coarse per-link sphere prune (prune=True)            */
-#define VMP_NO_EARLY_EXIT 4u /* dense mode: never stop a warp early (roofline runs)  */
+#define VMP_NO_EARLY_EXIT 4u /* dense mode: every test, no early exit, no broadphase  */
+#define VMP_NO_SPLIT 8u      /* never use the small-batch split kernel               */
+#define VMP_FORCE_SPLIT 32u  /* always use it (tests)                                */
 /* vmp_validate_motions flags (reference motion.py:38-90) */
 #define VMP_BACKWARD 16u     /* comb each stratum top-down (backward=True)            */
 

@@ -39,6 +39,7 @@ from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
 CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
+SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
 CODEGEN_VERSION = 7
 
 
@@ -162,7 +163,10 @@ def _state_function(lay: RobotLayout) -> str:
     emit = out.append
     emit("template <int STOP, bool PRUNE>")
     emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
-    emit("                                          int ns, int nc, int nb, bool ok) {")
+    emit("                                          int ns, int nc, int nb, bool ok,")
+    emit("                                          int sub = 0, int split = 1) {")
+    emit("  // split > 1: this thread handles obstacles k = sub (mod split) and self")
+    emit("  // pairs i = sub (mod split) of its configuration (small-batch kernels)")
     emit("  (void)env; (void)ns; (void)nc; (void)nb;")
     for line in _FK_BODY_PLACEHOLDER:
         emit(line)
@@ -179,10 +183,11 @@ def _state_function(lay: RobotLayout) -> str:
     # an edge, STOP 2) culls whole pair buckets with the group bounds below
     emit("  constexpr bool CULL_SELF = STOP == 2;")
     emit("  if constexpr (!CULL_SELF) {")
-    for sa, sb, thr in lay.pairs:
+    for pi, (sa, sb, thr) in enumerate(lay.pairs):
         ax, ay, az = _xyz(fine[sa])
         bx, by, bz = _xyz(fine[sb])
-        emit(f"    ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
+        emit(f"    if (sub == {pi} % split) "
+             f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
     emit("  }")
     # per-sphere constants
     for s in dyn:
@@ -297,16 +302,18 @@ def _state_function(lay: RobotLayout) -> str:
         rs2 = np.float32(np.float32(r) * np.float32(r))
         return f"{box_fn(r)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
 
-    def kind_loop(count: str, f4: str, loads: str, bound: str, radius: str, test_fn, coarse_fn):
+    def kind_loop(count: str, f4: str, base: str, loads: str, bound: str, radius: str, test_fn,
+                  coarse_fn):
         # dense mode (STOP 0): every obstacle, every test - the honest roofline run
+        emit(f"  p = {base} + sub * {f4};")
         emit("  if constexpr (!CULL) {")
-        emit(f"    for (int k = 0; k < {count}; ++k, p += {f4}) {{")
+        emit(f"    for (int k = sub; k < {count}; k += split, p += split * {f4}) {{")
         emit(f"      const float4 {loads};")
         group_tests(test_fn, coarse_fn, "      ")
         emit("    }")
         emit("  } else if constexpr (STOP == 1) {")
         # batch validation: one pass, a warp vote per obstacle on the group bounds
-        emit(f"    for (int k = 0; k < {count}; ++k, p += {f4}) {{")
+        emit(f"    for (int k = sub; k < {count}; k += split, p += split * {f4}) {{")
         emit(f"      const float4 {loads};")
         emit("      bool nr = false;")
         for gi, grp in enumerate(groups):
@@ -350,12 +357,12 @@ def _state_function(lay: RobotLayout) -> str:
 
     if dyn:
         emit("  const float4 *p = env;")
-        kind_loop("ns", "VMP_SPH_F4", "r0 = p[0], r1 = p[1]", "0", "pp[1].x", sph_test, sph_coarse)
-        emit("  p = env + VMP_SPH_F4 * ns;")
-        kind_loop("nc", "VMP_CAP_F4", "r0 = p[0], r1 = p[1], r2 = p[2]", "3", "pp[2].w",
-                  cap_test, cap_coarse)
-        emit("  p = env + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc;")
-        kind_loop("nb", "VMP_BOX_F4", "r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3]", "4", "pp[3].w",
+        kind_loop("ns", "VMP_SPH_F4", "env", "r0 = p[0], r1 = p[1]", "0", "pp[1].x",
+                  sph_test, sph_coarse)
+        kind_loop("nc", "VMP_CAP_F4", "(env + VMP_SPH_F4 * ns)", "r0 = p[0], r1 = p[1], r2 = p[2]",
+                  "3", "pp[2].w", cap_test, cap_coarse)
+        kind_loop("nb", "VMP_BOX_F4", "(env + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc)",
+                  "r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3]", "4", "pp[3].w",
                   box_test, box_coarse)
     emit("#undef VMP_STOP_NOW")
     emit("  return ok;")
@@ -441,10 +448,14 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_spheres(VmpFkArgs a
     if not lay.has_cc:
         return src
     src += f"""
-template <int PRUNE, int STOP, bool STAGED>
+template <int PRUNE, int STOP, bool STAGED, int SPLIT>
 __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
+  // SPLIT warps share one 32-configuration slice; warp w tests obstacles and
+  // self pairs w (mod SPLIT) and the partial verdict words are AND-ed in smem
+  // (more warps and a shorter critical path for latency-bound small batches)
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
+  __shared__ unsigned vmp_part[{BLOCK} / 32];
   const float4 *env = a.env.rec;
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
@@ -453,16 +464,31 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
     env = vmp_smem;
   }}
   const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
-  const long long stride = (long long)gridDim.x * {BLOCK};
-  for (long long base = blockIdx.x * (long long){BLOCK}; base < a.n; base += stride) {{
-    const long long i = base + threadIdx.x;
+  constexpr int TILE = {BLOCK} / SPLIT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = warp % SPLIT;
+  const long long stride = (long long)gridDim.x * TILE;
+  for (long long base = blockIdx.x * (long long)TILE; base < a.n; base += stride) {{
+    const long long i = base + (warp / SPLIT) * 32 + lane;
     const bool inr = i < a.n;
     const long long ii = inr ? i : a.n - 1;
     float q[{dofp}];
 {ld_q}
-    const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
+    const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear,
+                                                sub, SPLIT);
     const unsigned m = __ballot_sync(VMP_FULL, ok);
-    if ((threadIdx.x & 31) == 0 && inr) a.bits[i >> 5] = m;
+    if constexpr (SPLIT == 1) {{
+      if (lane == 0 && inr) a.bits[i >> 5] = m;
+    }} else {{
+      if (lane == 0) vmp_part[warp] = m;
+      __syncthreads();
+      if (sub == 0 && lane == 0 && inr) {{
+        unsigned word = m;
+#pragma unroll
+        for (int s = 1; s < SPLIT; ++s) word &= vmp_part[warp + s];
+        a.bits[i >> 5] = word;
+      }}
+      __syncthreads();
+    }}
   }}
 }}
 
@@ -592,9 +618,14 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     for prune in (0, 1):
         for staged in (0, 1):
             for stop in (0, 1):
+                g = "true" if staged else "false"
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                         f'vmp_validate_p{prune}_s{stop}_g{staged}(VmpValidateArgs a) '
-                        f'{{ vmp_validate_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
+                        f'{{ vmp_validate_body<{prune}, {stop}, {g}, 1>(a); }}\n')
+                if staged:
+                    src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
+                            f'vmp_validate_p{prune}_s{stop}_g1_x{SPLIT}(VmpValidateArgs a) '
+                            f'{{ vmp_validate_body<{prune}, {stop}, true, {SPLIT}>(a); }}\n')
             for stop in (1, 2):
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                         f'vmp_motion_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '

@@ -47,3 +47,21 @@ def test_config_validator_graph(cuda, early):
     q2 = workloads.uniform_configs(rob.limits, n, 77)
     cv(q2)
     assert np.array_equal(runtime.unpack_bits(cv().cpu().numpy(), n), ctx.validate_configs(q2))
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg4"])
+@pytest.mark.parametrize("early", [True, False])
+def test_split_kernel_matches_single_thread_kernel(cuda, cfg, early):
+    """The small-batch split kernel (4 warps per 32 configurations, obstacles and
+    self pairs partitioned) gives bit-identical verdict words."""
+    torch = cuda
+    wl = workloads.config1() if cfg == "cfg1" else workloads.config4(200_003)
+    rob = load_robot(wl.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    q = torch.from_numpy(wl.q).cuda()
+    n = q.shape[1]
+    words = {}
+    for split in (True, False):
+        words[split] = runtime.validate_device(ctx.module, ctx.device_env, q, n, q.stride(0),
+                                               early_exit=early, split=split).cpu().numpy()
+    assert np.array_equal(words[True], words[False])
