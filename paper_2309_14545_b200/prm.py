@@ -1,0 +1,202 @@
+"""Round-batched incremental PRM over the B200 validators.
+
+The reference PRM (pkg/src/vecmp/planners.py:243-291) draws ``prm_batch``
+Halton samples per round, checks each with ``ctx.state_valid`` and each of its
+``prm_k`` nearest-vertex edges with ``validate_motion_rake``, one call at a
+time.  Validity is order-independent, so a round maps onto two device calls:
+
+1. every sample of the round in one ``validate_batch`` launch;
+2. the k-NN edges of all valid samples in one ``validate_motions`` launch
+   (neighbour sets are still built sequentially on the host, so samples
+   earlier in the round are candidates for later ones, exactly as in the
+   reference).
+
+Vertices, adjacency lists and the shortest-path query are then updated in
+the reference's order, so the roadmap - and the returned waypoints - are the
+reference's whenever the verdicts are (tests/test_gpu_prm.py checks the
+waypoints against the reference's own runs).
+
+Host helpers restated from the reference: Halton draws (halton.py:17-67),
+exact k-NN with insertion-order ties (nn.py:18-69), uniform-cost search
+(planners.py:213-240).
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import runtime
+from .collision import ValidationContext
+from .motion import validate_motions
+
+
+def halton_bases(count: int) -> list[int]:
+    bases: list[int] = []
+    n = 2
+    while len(bases) < count:
+        if all(n % b for b in bases):
+            bases.append(n)
+        n += 1
+    return bases
+
+
+def radical_inverse(base: int, index: int) -> float:
+    """Base-``base`` digit reversal of ``index`` (same float64 accumulation
+    order as reference halton.py:27-40, so draws are bit-identical)."""
+    step = 1.0 / base
+    scale = step
+    acc = 0.0
+    while index > 0:
+        index, digit = divmod(index, base)
+        acc += digit * scale
+        scale *= step
+    return acc
+
+
+class HaltonDraws:
+    """Halton sequence scaled to joint limits, index starting at 1."""
+
+    def __init__(self, limits: np.ndarray):
+        self.lo = np.asarray(limits, dtype=np.float64)[:, 0]
+        self.hi = np.asarray(limits, dtype=np.float64)[:, 1]
+        self.bases = halton_bases(len(self.lo))
+        self.index = 1
+
+    def take(self, count: int) -> np.ndarray:
+        """(count, dof) float32 - the next ``count`` draws."""
+        out = np.empty((count, len(self.lo)), dtype=np.float32)
+        for r in range(count):
+            u = np.asarray([radical_inverse(b, self.index) for b in self.bases])
+            out[r] = (self.lo + u * (self.hi - self.lo)).astype(np.float32)
+            self.index += 1
+        return out
+
+
+class ExactNN:
+    """Insertion-ordered exact L2 neighbours (float32), ties to the earliest."""
+
+    def __init__(self, dim: int):
+        self.points = np.empty((dim, 0), dtype=np.float32)
+        self.count = 0
+
+    def add(self, q: np.ndarray) -> None:
+        if self.count == self.points.shape[1]:
+            grown = np.empty((self.points.shape[0], self.count + 64), dtype=np.float32)
+            grown[:, :self.count] = self.points[:, :self.count]
+            self.points = grown
+        self.points[:, self.count] = q
+        self.count += 1
+
+    def nearest_k(self, q: np.ndarray, k: int) -> list[tuple[int, float]]:
+        delta = self.points[:, :self.count] - q[:, None]
+        dist = np.sqrt(np.sum(delta * delta, axis=0, dtype=np.float32))
+        order = np.argsort(dist, kind="stable")[:k]
+        return [(int(i), float(dist[int(i)])) for i in order]
+
+
+def cheapest_route(adjacency: list, source: int, target: int) -> list[int] | None:
+    """Uniform-cost search; equal-cost ties resolved by heap order on (cost, vertex)."""
+    best = [float("inf")] * len(adjacency)
+    parent = [-1] * len(adjacency)
+    closed = [False] * len(adjacency)
+    best[source] = 0.0
+    frontier = [(0.0, source)]
+    while frontier:
+        cost, v = heapq.heappop(frontier)
+        if closed[v]:
+            continue
+        closed[v] = True
+        if v == target:
+            route = []
+            while v >= 0:
+                route.append(v)
+                v = parent[v]
+            return route[::-1]
+        for u, w in adjacency[v]:
+            c = cost + w
+            if c < best[u]:
+                best[u], parent[u] = c, v
+                heapq.heappush(frontier, (c, u))
+    return None
+
+
+@dataclass
+class PRMSettings:
+    """The reference PlannerSettings fields PRM reads (planners.py:31-45)."""
+
+    resolution: float = 0.02
+    max_iterations: int = 1_000_000
+    prm_k: int = 8
+    prm_batch: int = 128
+    rake_backward: bool = False
+    width: int = 8
+
+
+@dataclass
+class PRMResult:
+    waypoints: list | None
+    iterations: int
+    rounds: int
+    device_calls: int
+
+    @property
+    def success(self) -> bool:
+        return self.waypoints is not None
+
+
+def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> PRMResult:
+    """Incremental PRM with one state-validity launch and one motion launch per round."""
+    settings = settings or PRMSettings()
+    ctx = ValidationContext(robot.program, robot.model, robot.pairs, env, width=settings.width)
+    start = np.asarray(start, dtype=np.float32).reshape(-1)
+    goal = np.asarray(goal, dtype=np.float32).reshape(-1)
+    ends = ctx.validate_configs(np.stack([start, goal], axis=1))
+    if not ends[0]:
+        raise ValueError("start configuration is in collision")
+    if not ends[1]:
+        raise ValueError("goal configuration is in collision")
+    if np.array_equal(start, goal):
+        return PRMResult([start.copy(), goal.copy()], 0, 0, 1)
+    vertices = [start, goal]
+    adjacency: list[list[tuple[int, float]]] = [[], []]
+    nn = ExactNN(len(start))
+    nn.add(start)
+    nn.add(goal)
+    draws = HaltonDraws(robot.limits)
+    iterations = rounds = calls = 0
+    calls += 1
+    while iterations < settings.max_iterations:
+        count = min(settings.prm_batch, settings.max_iterations - iterations)
+        samples = draws.take(count)
+        iterations += count
+        rounds += 1
+        ok = ctx.validate_configs(np.ascontiguousarray(samples.T))       # launch 1
+        calls += 1
+        edges = []                                                         # (vid, nbr, dist)
+        for sample, valid in zip(samples, ok):
+            if not valid:
+                continue
+            nbrs = nn.nearest_k(sample, settings.prm_k)
+            vid = len(vertices)
+            vertices.append(sample)
+            adjacency.append([])
+            nn.add(sample)
+            edges.extend((vid, nbr, dist) for nbr, dist in nbrs)
+        if edges:
+            starts = np.stack([vertices[nbr] for _, nbr, _ in edges])
+            goals = np.stack([vertices[vid] for vid, _, _ in edges])
+            words = validate_motions(ctx, starts, goals, settings.resolution,
+                                     backward=settings.rake_backward)     # launch 2
+            calls += 1
+            free = runtime.unpack_bits(words.cpu().numpy(), len(edges))
+            for (vid, nbr, dist), edge_ok in zip(edges, free):
+                if edge_ok:
+                    adjacency[nbr].append((vid, dist))
+                    adjacency[vid].append((nbr, dist))
+        route = cheapest_route(adjacency, 0, 1)
+        if route is not None:
+            return PRMResult([vertices[v] for v in route], iterations, rounds, calls)
+    return PRMResult(None, iterations, rounds, calls)

@@ -296,10 +296,43 @@ def narrow() -> dict:
     return out
 
 
+def prm_cases() -> dict:
+    """Reference prm (planners.py:243-291) on the bundled problem sets."""
+    import time
+    from vecmp.planners import PlanningProblem, prm
+    from vecmp.problems import load_problem_set
+    from vecmp.resources import problem_set_path
+    out = {}
+    picks = (("toy_planar.yaml", "planar2", 3), ("arm_reach.yaml", "arm7", 2))
+    for fname, robot, stride in picks:
+        ps = load_problem_set(problem_set_path(fname))
+        for case in ps.problems[::stride]:
+            key = f"{robot}_{case.id}"
+            t0 = time.perf_counter()
+            res = prm(PlanningProblem(robot=ps.robot, env=case.env, start=case.start,
+                                      goal=case.goal), ps.settings)
+            dt = time.perf_counter() - t0
+            kinds, params = env_to_arrays(case.env)
+            out[f"env_{key}_kinds"], out[f"env_{key}_params"] = kinds, params
+            out[f"start_{key}"], out[f"goal_{key}"] = case.start, case.goal
+            s = ps.settings
+            out[f"settings_{key}"] = np.asarray([s.resolution, s.max_iterations, s.prm_k,
+                                                 s.prm_batch, float(s.rake_backward), s.width])
+            out[f"iterations_{key}"] = np.int64(res.iterations)
+            out[f"seconds_{key}"] = np.float64(dt)
+            out[f"path_{key}"] = (np.stack(res.path.waypoints) if res.success
+                                  else np.zeros((0, len(case.start)), np.float32))
+            print(f"  prm {key}: success={res.success} iterations={res.iterations} {dt:.2f} s")
+    return out
+
+
 def main() -> None:
     (HERE / "programs.json").write_text(json.dumps(programs(), indent=1, sort_keys=True) + "\n")
+    if len(sys.argv) > 1 and sys.argv[1] == "prm":
+        np.savez_compressed(HERE / "prm.npz", **prm_cases())
+        return
     for name, fn in (("fk", fk), ("blocks", blocks), ("motion", motion), ("lanes", lanes),
-                     ("narrow", narrow)):
+                     ("narrow", narrow), ("prm", prm_cases)):
         np.savez_compressed(HERE / f"{name}.npz", **fn())
         print("wrote", name)
 

@@ -34,6 +34,30 @@ def test_motion_validator_graph_matches_eager_and_oracle(cuda):
         assert bool(v.all()) == bool(eager[i])
 
 
+def test_motion_pipeline_overlapped_batches(cuda):
+    torch = cuda
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    E = 1024
+    batches = []
+    rng = np.random.default_rng(4)
+    for _ in range(6):
+        idx = rng.choice(len(mw.starts), E, replace=False)
+        batches.append((torch.from_numpy(mw.starts[idx]).pin_memory(),
+                        torch.from_numpy(mw.goals[idx]).pin_memory()))
+    expect = [runtime.unpack_bits(M.validate_motions(ctx, s, g, mw.resolution).cpu().numpy(), E)
+              for s, g in batches]
+    pipe = M.MotionPipeline(ctx, E, mw.resolution)
+    prev = None
+    for k, (s, g) in enumerate(batches):
+        t = pipe.submit(s, g)
+        if prev is not None:
+            assert runtime.unpack_bits(pipe.result(prev), E).tolist() == expect[k - 1].tolist()
+        prev = t
+    assert runtime.unpack_bits(pipe.result(prev), E).tolist() == expect[-1].tolist()
+
+
 @pytest.mark.parametrize("early", [True, False])
 def test_config_validator_graph(cuda, early):
     wl = workloads.config3(1 << 16)
