@@ -135,6 +135,28 @@ int vmp_sphere_hits(const vmp_env *env, const float *xyz, int64_t n, int64_t ld,
 int vmp_pair_clear(const float *a, const float *b, int64_t n, int64_t ld, float thr,
                    uint8_t *clear, void *stream);
 
+/* Exact k-nearest neighbours (reference NNIndex.k_nearest / nearest,
+ * nn.py:45-69).  points: dim x ld float32 SoA (device), n_points columns;
+ * queries: n_queries x qld float32 rows (device).  Distance = sqrtf of the
+ * float32 squares summed in joint order (unfused); results ascending by
+ * (distance, point index) - ties go to the earlier-inserted point.
+ *   visible   : optional device int64 per query - only points [0, visible[q])
+ *               are candidates (a growing index queried mid-insertion)
+ *   out_index : n_queries x k int32, -1 past the candidate count
+ *   out_dist  : n_queries x k float32, +inf past the candidate count
+ * 1 <= k <= VMP_KNN_MAX_K, 1 <= dim <= VMP_KNN_MAX_DIM. */
+#define VMP_KNN_MAX_K 32
+#define VMP_KNN_MAX_DIM 64
+int vmp_knn(const float *points, int64_t n_points, int64_t ld, int32_t dim, const float *queries,
+            int64_t n_queries, int64_t qld, const int64_t *visible, int32_t k, int32_t *out_index,
+            float *out_dist, void *stream);
+
+/* Every query-to-point distance (same arithmetic as vmp_knn) into out
+ * (n_queries x ldo); the k > VMP_KNN_MAX_K path sorts these stably. */
+int vmp_nn_distances(const float *points, int64_t n_points, int64_t ld, int32_t dim,
+                     const float *queries, int64_t n_queries, int64_t qld, float *out, int64_t ldo,
+                     void *stream);
+
 /* Select the CUDA device used by subsequent vmp calls on this thread (robots
  * and environments remember the device they were created on). */
 int vmp_set_device(int32_t device);

@@ -28,6 +28,8 @@ Reference functions restated (file:line in /root/reference/pkg/src/vecmp):
   interpolate_lanes, rake        lanes.py:91-103, motion.py:32-78
   float64 FK                     trace.py:100-137 (graph semantics)
   float64 distance oracles       pkg/tests/test_collision.py:24-39,136-159
+  exact k-NN scan                nn.py:45-69 (float32 joint-order sum, stable
+                                 argsort: ties to the first-inserted point)
 """
 
 from __future__ import annotations
@@ -444,3 +446,20 @@ def rake_blocks_from_states(valid: np.ndarray, width: int, backward: bool = Fals
     j = (bad - 1) % s + 1                      # position inside its stratum
     it = (s - j + 1) if backward else j
     return False, int(it.min())
+
+
+# ------------------------------------------------------------ nearest neighbours
+
+def nn_distances(points: np.ndarray, q) -> np.ndarray:
+    """Distances of q to the (dim, n) float32 SoA points (nn.py:45-51)."""
+    qv = np.asarray(q, dtype=F32).reshape(-1)
+    diff = np.asarray(points, dtype=F32) - qv[:, None]
+    return np.sqrt(np.sum(diff * diff, axis=0, dtype=F32))
+
+
+def nn_k_nearest(points: np.ndarray, q, k: int) -> tuple[np.ndarray, np.ndarray]:
+    """(indices, distances) of the k closest, ascending, ties to the smaller
+    index (nn.py:60-69 stable argsort)."""
+    d = nn_distances(points, q)
+    order = np.argsort(d, kind="stable")[:k]
+    return order, d[order]

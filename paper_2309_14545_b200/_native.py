@@ -42,7 +42,10 @@ EXPORTS = (
     "vmp_env_create", "vmp_env_destroy", "vmp_env_bytes", "vmp_fk_rows", "vmp_fk_spheres",
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
+    "vmp_knn", "vmp_nn_distances",
 )
+VMP_KNN_MAX_K = 32
+VMP_KNN_MAX_DIM = 64
 
 
 class RobotDesc(ctypes.Structure):
@@ -106,6 +109,10 @@ def lib() -> ctypes.CDLL:
         "vmp_discretize": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, vp, vp], ctypes.c_int),
         "vmp_sphere_hits": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),
         "vmp_pair_clear": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),
+        "vmp_knn": ([vp, c_i64, c_i64, c_i32, vp, c_i64, c_i64, vp, c_i32, vp, vp, vp],
+                    ctypes.c_int),
+        "vmp_nn_distances": ([vp, c_i64, c_i64, c_i32, vp, c_i64, c_i64, vp, c_i64, vp],
+                             ctypes.c_int),
         "vmp_set_device": ([c_i32], ctypes.c_int),
         "vmp_device_info": ([ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)], ctypes.c_int),
     }

@@ -17,21 +17,24 @@ from __future__ import annotations
 
 import importlib
 
-from . import collision, motion, program
+from . import collision, motion, program, simplify
 
 #: module -> names to rebind (only where the module actually defines them)
 TARGETS = {
     "": ("evaluate_program", "validate_block", "ValidationContext", "sphere_vs_sphere_lanes",
          "sphere_vs_capsule_lanes", "sphere_vs_cuboid_lanes", "discretization_count",
-         "raked_motion_check", "validate_motion_rake"),
+         "raked_motion_check", "validate_motion_rake", "shortcut", "bspline_smooth",
+         "simplify_path"),
     "program": ("evaluate_program",),
     "collision": ("evaluate_program", "validate_block", "ValidationContext",
                   "sphere_vs_sphere_lanes", "sphere_vs_capsule_lanes", "sphere_vs_cuboid_lanes"),
     "motion": ("ValidationContext", "discretization_count", "raked_motion_check",
                "validate_motion_rake"),
     "planners": ("ValidationContext", "validate_motion_rake"),
-    "simplify": ("ValidationContext", "validate_motion_rake"),
-    "cli": ("ValidationContext", "validate_motion_rake"),
+    "simplify": ("ValidationContext", "validate_motion_rake", "shortcut", "bspline_smooth",
+                 "simplify_path"),
+    "cli": ("ValidationContext", "validate_motion_rake", "simplify_path"),
+    "bench": ("simplify_path",),
 }
 
 REPLACEMENTS = {
@@ -44,6 +47,10 @@ REPLACEMENTS = {
     "discretization_count": motion.discretization_count,
     "raked_motion_check": motion.raked_motion_check,
     "validate_motion_rake": motion.validate_motion_rake,
+    # batched speculative simplifier: same waypoints, motion checks in launches
+    "shortcut": simplify.shortcut,
+    "bspline_smooth": simplify.bspline_smooth,
+    "simplify_path": simplify.simplify_path,
 }
 
 _SAVED: dict = {}

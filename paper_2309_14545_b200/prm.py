@@ -3,13 +3,14 @@
 The reference PRM (pkg/src/vecmp/planners.py:243-291) draws ``prm_batch``
 Halton samples per round, checks each with ``ctx.state_valid`` and each of its
 ``prm_k`` nearest-vertex edges with ``validate_motion_rake``, one call at a
-time.  Validity is order-independent, so a round maps onto two device calls:
+time.  Validity is order-independent, so a round maps onto three device calls:
 
 1. every sample of the round in one ``validate_batch`` launch;
-2. the k-NN edges of all valid samples in one ``validate_motions`` launch
-   (neighbour sets are still built sequentially on the host, so samples
-   earlier in the round are candidates for later ones, exactly as in the
-   reference).
+2. the k nearest vertices of every valid sample in one exact k-NN launch
+   (nn.NNIndex.k_nearest_many); sample j only sees the vertices inserted
+   before it - the ones before the round plus the valid samples before j -
+   exactly as the reference's insert-after-query loop;
+3. the k-NN edges of all valid samples in one ``validate_motions`` launch.
 
 Vertices, adjacency lists and the shortest-path query are then updated in
 the reference's order, so the roadmap - and the returned waypoints - are the
@@ -17,8 +18,7 @@ reference's whenever the verdicts are (tests/test_gpu_prm.py checks the
 waypoints against the reference's own runs).
 
 Host helpers restated from the reference: Halton draws (halton.py:17-67),
-exact k-NN with insertion-order ties (nn.py:18-69), uniform-cost search
-(planners.py:213-240).
+uniform-cost search (planners.py:213-240).
 """
 
 from __future__ import annotations
@@ -31,6 +31,7 @@ import numpy as np
 from . import runtime
 from .collision import ValidationContext
 from .motion import validate_motions
+from .nn import NNIndex
 
 
 def halton_bases(count: int) -> list[int]:
@@ -73,28 +74,6 @@ class HaltonDraws:
             out[r] = (self.lo + u * (self.hi - self.lo)).astype(np.float32)
             self.index += 1
         return out
-
-
-class ExactNN:
-    """Insertion-ordered exact L2 neighbours (float32), ties to the earliest."""
-
-    def __init__(self, dim: int):
-        self.points = np.empty((dim, 0), dtype=np.float32)
-        self.count = 0
-
-    def add(self, q: np.ndarray) -> None:
-        if self.count == self.points.shape[1]:
-            grown = np.empty((self.points.shape[0], self.count + 64), dtype=np.float32)
-            grown[:, :self.count] = self.points[:, :self.count]
-            self.points = grown
-        self.points[:, self.count] = q
-        self.count += 1
-
-    def nearest_k(self, q: np.ndarray, k: int) -> list[tuple[int, float]]:
-        delta = self.points[:, :self.count] - q[:, None]
-        dist = np.sqrt(np.sum(delta * delta, axis=0, dtype=np.float32))
-        order = np.argsort(dist, kind="stable")[:k]
-        return [(int(i), float(dist[int(i)])) for i in order]
 
 
 def cheapest_route(adjacency: list, source: int, target: int) -> list[int] | None:
@@ -162,9 +141,9 @@ def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> 
         return PRMResult([start.copy(), goal.copy()], 0, 0, 1)
     vertices = [start, goal]
     adjacency: list[list[tuple[int, float]]] = [[], []]
-    nn = ExactNN(len(start))
-    nn.add(start)
-    nn.add(goal)
+    nn = NNIndex(len(start))
+    nn.insert(start, 0)
+    nn.insert(goal, 1)
     draws = HaltonDraws(robot.limits)
     iterations = rounds = calls = 0
     calls += 1
@@ -176,20 +155,24 @@ def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> 
         ok = ctx.validate_configs(np.ascontiguousarray(samples.T))       # launch 1
         calls += 1
         edges = []                                                         # (vid, nbr, dist)
-        for sample, valid in zip(samples, ok):
-            if not valid:
-                continue
-            nbrs = nn.nearest_k(sample, settings.prm_k)
-            vid = len(vertices)
-            vertices.append(sample)
-            adjacency.append([])
-            nn.add(sample)
-            edges.extend((vid, nbr, dist) for nbr, dist in nbrs)
+        fresh = samples[ok]
+        if len(fresh):
+            # sample j of the round sees the vertices inserted before it
+            base = len(vertices)
+            nn.insert_many(fresh, range(base, base + len(fresh)))
+            nbr, dist = nn.k_nearest_many(fresh, settings.prm_k,                # launch 2
+                                          visible=base + np.arange(len(fresh)))
+            calls += 1
+            for j, sample in enumerate(fresh):
+                vertices.append(sample)
+                adjacency.append([])
+                edges.extend((base + j, int(b), float(d)) for b, d in zip(nbr[j], dist[j])
+                             if b >= 0)
         if edges:
             starts = np.stack([vertices[nbr] for _, nbr, _ in edges])
             goals = np.stack([vertices[vid] for vid, _, _ in edges])
             words = validate_motions(ctx, starts, goals, settings.resolution,
-                                     backward=settings.rake_backward)     # launch 2
+                                     backward=settings.rake_backward)     # launch 3
             calls += 1
             free = runtime.unpack_bits(words.cpu().numpy(), len(edges))
             for (vid, nbr, dist), edge_ok in zip(edges, free):

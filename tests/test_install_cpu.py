@@ -29,8 +29,9 @@ def vecmp_pkg():
 
 def test_patch_rebinds_all_import_sites(vecmp_pkg):
     from paper_2309_14545_b200 import collision, install, motion, program
+    from paper_2309_14545_b200 import simplify as batched
     done = install.patch_vecmp(vecmp_pkg)
-    assert len(done) == 26
+    assert len(done) == 34
     planners = importlib.import_module("vecmp.planners")
     simplify = importlib.import_module("vecmp.simplify")
     cli = importlib.import_module("vecmp.cli")
@@ -38,6 +39,9 @@ def test_patch_rebinds_all_import_sites(vecmp_pkg):
     assert planners.validate_motion_rake is motion.validate_motion_rake
     assert simplify.validate_motion_rake is motion.validate_motion_rake
     assert cli.ValidationContext is collision.ValidationContext
+    assert cli.simplify_path is batched.simplify_path
+    assert importlib.import_module("vecmp.bench").simplify_path is batched.simplify_path
+    assert vecmp_pkg.shortcut is batched.shortcut and simplify.bspline_smooth is batched.bspline_smooth
     assert vecmp_pkg.program.evaluate_program is program.evaluate_program
     assert vecmp_pkg.collision.validate_block is collision.validate_block
     install.unpatch_vecmp(vecmp_pkg)
