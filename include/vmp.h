@@ -118,7 +118,8 @@ int vmp_validate_motions(const vmp_robot *robot, const vmp_env *env, const float
 int64_t vmp_motion_workspace_bytes(int64_t n_edges);
 
 /* n = max(1, ceil(||g - s|| / resolution)) per edge with numpy float32
- * reduction order (reference motion.py:25-29, lanes.py:106-113). */
+ * reduction order (reference motion.py:25-29, lanes.py:106-113); dim <= 128
+ * (numpy sums longer rows recursively). */
 int vmp_discretize(const float *starts, const float *goals, int64_t n_edges, int32_t dim,
                    int64_t sld, double resolution, int32_t *n_out, void *stream);
 

@@ -40,7 +40,7 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
 SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
-CODEGEN_VERSION = 7
+CODEGEN_VERSION = 8
 
 
 def f32_literal(value: float) -> str:
@@ -512,7 +512,6 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   }}
   const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
   const int lane = threadIdx.x & 31;
-  const long long W = a.width;
   // programmatic dependent launch: everything above (env staging, const check)
   // overlapped the plan kernel; wait for its results here
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -562,7 +561,8 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     }}
     const int4 rank = __ldcg(a.order + ri);                 // (edge, n, chunks, 0)
     const long long ei = rank.x;
-    const long long first_iter = (32 * ci) / W + 1;
+    const unsigned Wu = (unsigned)a.width;   // 32-bit rake index math (n < 2^31, positions
+    const unsigned first_iter = (32u * (unsigned)ci) / Wu + 1;   // < 2^31 guarded by the plan)
     const int chunks = rank.z;
     const int failed = __ldcg(a.fail_of + ei);
     const long long n = rank.y;
@@ -573,14 +573,12 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
         s[j] = __ldg(a.starts + ei * a.sld + j);
         g[j] = __ldg(a.goals + ei * a.sld + j);
       }}
-      // 32-bit rake index math (n < 2^31, positions < 2^31 guarded by the plan)
-      const unsigned Wu = (unsigned)a.width;
-      const unsigned S = (unsigned)((n + W - 1) / W);
+      const unsigned S = vmp_ceil_div((unsigned)n, Wu);
       const unsigned p = 32u * (unsigned)ci + lane;
       const unsigned j = p / Wu + 1;
       const unsigned k = p - (j - 1) * Wu;
       const long long idx = (long long)k * S + (a.backward ? (S - j + 1) : j);
-      const bool inr = (long long)p < (long long)S * W && idx <= n;
+      const bool inr = (unsigned long long)p < (unsigned long long)S * Wu && idx <= n;
       const float tt = vmp_rake_param(inr ? idx : 1, n);
       float q[{dofp}];
 #pragma unroll
@@ -588,7 +586,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
       if (bad && lane == 0)
-        atomicMin(a.fail_of + ei, (int)((32 * ci + __ffs(bad) - 1) / W + 1));
+        atomicMin(a.fail_of + ei, (int)((32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1));
     }}
   }}
   if (a.fused_finalize) {{                  // the last CTA to finish writes the outputs

@@ -256,6 +256,15 @@ __device__ __forceinline__ float vmp_lerp_exact(float s, float g, float t) {
   return __fadd_rn(s, __fmul_rn(t, __fsub_rn(g, s)));
 }
 
+/* ceil(n / w) and the number of 32-position chunks of a W-lane rake over n
+ * states, with 32-bit division (n < 2^31, w >= 1). */
+__device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w) {
+  return n / w + (n % w != 0u);
+}
+__device__ __forceinline__ unsigned vmp_rake_chunks(unsigned n, unsigned w) {
+  return (unsigned)(((unsigned long long)vmp_ceil_div(n, w) * w + 31ull) >> 5);
+}
+
 /* Motion outputs from the per-edge plan: verdict bit (no failure recorded),
  * n, and the W-rake block count (failing iteration, or S = ceil(n / W)).
  * Threads [tid0, tid0 + nthreads) of a group; nthreads a multiple of 32. */
@@ -273,7 +282,7 @@ __device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width,
       if ((tid & 31) == 0) bits[e >> 5] = m;
       const long long n = __ldcg(n_of + e);
       if (n_states) n_states[e] = (int)n;
-      if (blocks) blocks[e] = ok ? (int)((n + width - 1) / width) : fail;
+      if (blocks) blocks[e] = ok ? (int)vmp_ceil_div((unsigned)n, (unsigned)width) : fail;
     }
   }
 }
