@@ -44,7 +44,7 @@ typedef struct {
   unsigned int max_chunks;        /* max over edges of ceil(S W / 32), S = ceil(n / W) */
   unsigned int n_big;             /* edges with chunks >= VMP_HBINS - 1 */
   unsigned int done_ctas;         /* CTAs of the rake kernel that finished */
-  unsigned int plan_done;         /* CTAs of the fused plan kernel that finished */
+  unsigned int plan_done;         /* reserved (kept zero) */
   unsigned int pad_[2];           /* keep the arrays behind 16-byte aligned */
 } VmpMotionHeader;
 

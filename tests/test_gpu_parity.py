@@ -329,3 +329,25 @@ def test_motion_repeated_calls_consistent(cuda):
     for i in range(len(s)):
         assert M.raked_motion_check(s[i], g[i], ctx, res) == (
             bool(fx[f"verdict_{key}_w8_b0"][i]), int(fx[f"blocks_{key}_w8_b0"][i]))
+
+
+@pytest.mark.parametrize("tiles", [1, 3, 17])   # 4,096 / 12,288 / 69,632 edges
+def test_motion_plan_paths_agree(cuda, tiles):
+    """The three plan paths (one edge per cluster thread up to 8,192 edges,
+    eight per thread up to 65,536, multi-kernel plan above) give the verdicts,
+    n and W-block counts of the oracle-checked 4,096-edge config 2 batch."""
+    mw = workloads.config2()
+    rob = load_robot("arm7")
+    for width in (32, 8):
+        ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env, width=width)
+        ref = M.validate_motions(ctx, mw.starts, mw.goals, mw.resolution, width=width, counts=True)
+        ref_v = runtime.unpack_bits(ref[0].cpu().numpy(), len(mw.starts))
+        s, g = np.tile(mw.starts, (tiles, 1)), np.tile(mw.goals, (tiles, 1))
+        ws = runtime.motion_workspace(len(s))
+        for _ in range(2):                              # fresh, then reused workspace
+            b, n, blk = M.validate_motions(ctx, s, g, mw.resolution, width=width, counts=True,
+                                           workspace=ws)
+            assert runtime.unpack_bits(b.cpu().numpy(), len(s)).tolist() == \
+                np.tile(ref_v, tiles).tolist()
+            assert n.cpu().numpy().tolist() == np.tile(ref[1].cpu().numpy(), tiles).tolist()
+            assert blk.cpu().numpy().tolist() == np.tile(ref[2].cpu().numpy(), tiles).tolist()
