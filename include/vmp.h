@@ -37,6 +37,7 @@ extern "C" {
 #define VMP_NO_EARLY_EXIT 4u /* dense mode: every test, no early exit, no broadphase  */
 #define VMP_NO_SPLIT 8u      /* never use the small-batch split kernel               */
 #define VMP_FORCE_SPLIT 32u  /* always use it (tests)                                */
+#define VMP_TWO_PASS 64u     /* two-pass broadphase (bound mask per 32 obstacles)     */
 /* vmp_validate_motions flags (reference motion.py:38-90) */
 #define VMP_BACKWARD 16u     /* comb each stratum top-down (backward=True)            */
 

@@ -28,6 +28,7 @@ VMP_PRUNE = 1
 VMP_NO_EARLY_EXIT = 4
 VMP_NO_SPLIT = 8
 VMP_FORCE_SPLIT = 32
+VMP_TWO_PASS = 64
 VMP_BACKWARD = 16
 
 NVCC_FLAGS = [

@@ -40,7 +40,7 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
 SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
-CODEGEN_VERSION = 8
+CODEGEN_VERSION = 10
 
 
 def f32_literal(value: float) -> str:
@@ -161,10 +161,11 @@ def _state_function(lay: RobotLayout) -> str:
     dyn = lay.dynamic
     out = []
     emit = out.append
-    emit("template <int STOP, bool PRUNE>")
+    emit("template <int STOP, bool PRUNE, bool TWO = (STOP == 2)>")
     emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
     emit("                                          int ns, int nc, int nb, bool ok,")
-    emit("                                          int sub = 0, int split = 1) {")
+    emit("                                          int sub = 0, int split = 1,")
+    emit("                                          unsigned long long *bar = nullptr) {")
     emit("  // split > 1: this thread handles obstacles k = sub (mod split) and self")
     emit("  // pairs i = sub (mod split) of its configuration (small-batch kernels)")
     emit("  (void)env; (void)ns; (void)nc; (void)nb;")
@@ -311,7 +312,7 @@ def _state_function(lay: RobotLayout) -> str:
         emit(f"      const float4 {loads};")
         group_tests(test_fn, coarse_fn, "      ")
         emit("    }")
-        emit("  } else if constexpr (STOP == 1) {")
+        emit("  } else if constexpr (STOP == 1 && !TWO) {")
         # batch validation: one pass, a warp vote per obstacle on the group bounds
         emit(f"    for (int k = sub; k < {count}; k += split, p += split * {f4}) {{")
         emit(f"      const float4 {loads};")
@@ -326,15 +327,17 @@ def _state_function(lay: RobotLayout) -> str:
         emit("      if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
         emit("    }")
         emit("  } else {")
-        # motion rake, two passes per 32 obstacles: (1) branch-free bound tests
-        # of every group against every obstacle bound into a per-lane bit mask,
-        # (2) one warp OR, then full tests only for obstacles near some lane.
-        # Exact: an obstacle lies inside its bound, every sphere inside its group bound.
-        emit(f"    for (int k0 = 0; k0 < {count}; k0 += 32, p += 32 * {f4}) {{")
-        emit(f"      const int kn = min(32, {count} - k0);")
+        # motion rake and latency-bound small batches (TWO), two passes per 32
+        # obstacles: (1) branch-free bound tests of every group against every
+        # obstacle bound into a per-lane bit mask, (2) one warp OR, then full
+        # tests only for obstacles near some lane.  Exact: an obstacle lies
+        # inside its bound, every sphere inside its group bound.  With split > 1
+        # this thread's obstacles are k = sub (mod split).
+        emit(f"    for (int k0 = sub; k0 < {count}; k0 += 32 * split, p += 32 * split * {f4}) {{")
+        emit(f"      const int kn = min(32, ({count} - k0 + split - 1) / split);")
         emit("      unsigned near = 0;")
         emit("      for (int j = 0; j < kn; ++j) {")
-        emit(f"        const float4 *pp = p + j * {f4};")
+        emit(f"        const float4 *pp = p + j * split * {f4};")
         emit(f"        const float4 bnd = pp[{bound}];")
         emit(f"        const float brad = {radius};")
         emit("        bool nr = false;")
@@ -347,7 +350,7 @@ def _state_function(lay: RobotLayout) -> str:
         emit("      while (todo) {")
         emit("        const int j = __ffs(todo) - 1;")
         emit("        todo &= todo - 1;")
-        emit(f"        const float4 *pp = p + j * {f4};")
+        emit(f"        const float4 *pp = p + j * split * {f4};")
         emit(f"        const float4 {loads.replace('p[', 'pp[')};")
         group_tests(test_fn, coarse_fn, "        ")
         emit("        if (VMP_STOP_NOW) return ok;")
@@ -356,6 +359,8 @@ def _state_function(lay: RobotLayout) -> str:
         emit("  }")
 
     if dyn:
+        # the environment copy (cp.async.bulk) was in flight during FK and self pairs
+        emit("  if (bar) vmp_mbar_wait(bar, 0);")
         emit("  const float4 *p = env;")
         kind_loop("ns", "VMP_SPH_F4", "env", "r0 = p[0], r1 = p[1]", "0", "pp[1].x",
                   sph_test, sph_coarse)
@@ -448,7 +453,7 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_spheres(VmpFkArgs a
     if not lay.has_cc:
         return src
     src += f"""
-template <int PRUNE, int STOP, bool STAGED, int SPLIT>
+template <int PRUNE, int STOP, bool STAGED, int SPLIT, bool TWO = false>
 __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   // SPLIT warps share one 32-configuration slice; warp w tests obstacles and
   // self pairs w (mod SPLIT) and the partial verdict words are AND-ed in smem
@@ -456,14 +461,14 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
   __shared__ unsigned vmp_part[{BLOCK} / 32];
-  const float4 *env = a.env.rec;
+  // the environment copy overlaps the joint loads, FK and self pairs of the
+  // first tile; vmp_state waits for it before the first obstacle
+  const float4 *env = STAGED ? vmp_smem : a.env.rec;
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
     __syncthreads();
-    vmp_mbar_wait(&vmp_bar, 0);
-    env = vmp_smem;
   }}
-  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+  bool cclear = true, cdone = false;
   constexpr int TILE = {BLOCK} / SPLIT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = warp % SPLIT;
   const long long stride = (long long)gridDim.x * TILE;
@@ -473,8 +478,14 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
     const long long ii = inr ? i : a.n - 1;
     float q[{dofp}];
 {ld_q}
-    const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear,
-                                                sub, SPLIT);
+    bool ok = vmp_state<STOP, PRUNE != 0, TWO>(q, env, a.env.ns, a.env.nc, a.env.nb, inr, sub,
+                                               SPLIT, STAGED ? &vmp_bar : nullptr);
+    if (!cdone) {{                            // CTA-uniform: once, after the first tile
+      if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
+      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+      cdone = true;
+    }}
+    ok = ok && cclear;
     const unsigned m = __ballot_sync(VMP_FULL, ok);
     if constexpr (SPLIT == 1) {{
       if (lane == 0 && inr) a.bits[i >> 5] = m;
@@ -490,6 +501,7 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
       __syncthreads();
     }}
   }}
+  if (STAGED && !cdone) vmp_mbar_wait(&vmp_bar, 0);   // no tile: still retire the copy
 }}
 
 template <int PRUNE, int STOP, bool STAGED>
@@ -624,6 +636,11 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
                     src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                             f'vmp_validate_p{prune}_s{stop}_g1_x{SPLIT}(VmpValidateArgs a) '
                             f'{{ vmp_validate_body<{prune}, {stop}, true, {SPLIT}>(a); }}\n')
+                if staged and stop == 1:            # two-pass broadphase, small batches
+                    for sp in (1, SPLIT):
+                        src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
+                                f'vmp_validate_p{prune}_s1_g1_x{sp}t(VmpValidateArgs a) '
+                                f'{{ vmp_validate_body<{prune}, 1, true, {sp}, true>(a); }}\n')
             for stop in (1, 2):
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                         f'vmp_motion_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '

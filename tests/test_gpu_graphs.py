@@ -89,3 +89,22 @@ def test_split_kernel_matches_single_thread_kernel(cuda, cfg, early):
         words[split] = runtime.validate_device(ctx.module, ctx.device_env, q, n, q.stride(0),
                                                early_exit=early, split=split).cpu().numpy()
     assert np.array_equal(words[True], words[False])
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg3", "cfg4"])
+def test_every_kernel_variant_gives_the_same_words(cuda, cfg):
+    """Single-thread / split, one-pass / two-pass broadphase, early exit /
+    dense: six kernels, bit-identical verdict words (the product path picks
+    among them by batch size and scene; the oracle checks the product path)."""
+    torch = cuda
+    n = 70_001
+    wl = {"cfg1": workloads.config1, "cfg3": workloads.config3, "cfg4": workloads.config4}[cfg](n)
+    rob = load_robot(wl.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    q = torch.from_numpy(wl.q).cuda()
+    ref = ctx.validate_batch(q).cpu().numpy()
+    for kw in (dict(split=False), dict(split=True), dict(split=False, two_pass=True),
+               dict(split=True, two_pass=True), dict(split=False, early_exit=False),
+               dict(split=True, early_exit=False)):
+        got = runtime.validate_device(ctx.module, ctx.device_env, q, n, q.stride(0), **kw)
+        assert np.array_equal(got.cpu().numpy(), ref), kw
