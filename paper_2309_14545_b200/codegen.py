@@ -40,7 +40,24 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
 SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
-CODEGEN_VERSION = 10
+FK_SMEM_TILE = 160 * 1024   # largest vmp_fk_spheres centre tile (shared memory bytes)
+
+
+def fk_tiling(n_rows: int) -> tuple[int, int]:
+    """(configurations per thread, tile buffers) of vmp_fk_spheres.
+
+    Longer contiguous row segments per bulk store write faster (measured,
+    scripts/exp_fk_tile.py: 0.83 -> 0.91 of HBM from 1 KB to 2 KB rows for
+    arm7), so take the largest 1 / 2 / 4 configurations per thread whose tile
+    fits; double-buffer when two tiles fit in 80 KB.  0 buffers: the rows do
+    not fit at all and the kernel uses streaming stores only.
+    """
+    for per in (4, 2, 1):
+        tile_bytes = n_rows * BLOCK * per * 4
+        if tile_bytes <= FK_SMEM_TILE:
+            return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
+    return 1, 0
+CODEGEN_VERSION = 15
 
 
 def f32_literal(value: float) -> str:
@@ -411,6 +428,14 @@ def _kernels(lay: RobotLayout, program) -> str:
         for c, v in enumerate(marker.xyz):
             centre_rows.append(f"    __stcs(o + {3 * m + c} * a.ldo, v{int(v)});")
     centre_rows = "\n".join(centre_rows)
+    n_rows = 3 * len(program.checks)
+    # two tile buffers when they fit in 80 KB (>= 2 CTAs per SM), else one; the
+    # host's fk_tile_bytes (csrc/vmp.cu) applies the same rule
+    per, nbuf = fk_tiling(n_rows)
+    tile = BLOCK * per
+    smem_rows = "\n".join(f"        s[{3 * m + c} * {tile} + c] = v{int(v)};"
+                           for m, marker in enumerate(program.checks)
+                           for c, v in enumerate(marker.xyz))
     src = f"""
 extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_rows(VmpFkArgs a) {{
   for (long long i = blockIdx.x * (long long){BLOCK} + threadIdx.x; i < a.n;
@@ -424,30 +449,72 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_rows(VmpFkArgs a) {
   }}
 }}
 
+// shared memory vmp_fk_spheres needs (read by the host after loading the module)
+extern "C" __device__ const int vmp_fk_smem_bytes = {max(nbuf, 1) * n_rows * tile * 4 if nbuf else 0};
+
 extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_spheres(VmpFkArgs a) {{
-  // HBM-bound: the next configuration's joints are prefetched while this one's
-  // centres are computed; centres leave with streaming (evict-first) stores
-  const long long stride = (long long)gridDim.x * {BLOCK};
-  long long i = blockIdx.x * (long long){BLOCK} + threadIdx.x;
-  float qn[{dofp}];
-  if (i < a.n) {{
-    const long long ii = i;
-    float *q = qn;
-{ld_q}
-  }}
-  for (; i < a.n; i += stride) {{
-    float q[{dofp}];
+  // HBM-bound (write side): a CTA computes the centres of a {tile}-configuration
+  // tile ({per} per thread, all joints loaded up front) into shared
+  // memory ({n_rows} rows x {tile} floats, {nbuf} buffer(s)) and each row leaves as
+  // ONE contiguous {tile * 4} B cp.async.bulk (TMA) store that overlaps the next
+  // tile's FK.  Unaligned outputs and the partial last tile use streaming stores.
+  extern __shared__ float vmp_rows[];                  // [{max(nbuf, 1)}][{n_rows}][{tile}]
+  const bool bulk = {"true" if nbuf else "false"} && (a.ldo & 3) == 0 &&
+                    ((unsigned long long)a.out & 15) == 0;
+  const long long ntiles = (a.n + {tile} - 1) / {tile};
+  int buf = 0;
+  float qn[{per}][{dofp}];               // next tile's joints, prefetched
+  if (blockIdx.x < ntiles) {{
 #pragma unroll
-    for (int j = 0; j < {dofp}; ++j) q[j] = qn[j];
-    if (i + stride < a.n) {{
-      const long long ii = i + stride;
-      float *q = qn;
+    for (int r = 0; r < {per}; ++r) {{
+      const long long ii = min((long long)blockIdx.x * {tile} + r * {BLOCK} + threadIdx.x, a.n - 1);
+      float *q = qn[r];
 {ld_q}
     }}
-    VMP_FK_BODY
-    float *o = a.out + i;
-{centre_rows}
   }}
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf = (buf + 1) % {max(nbuf, 1)}) {{
+    const long long base = tile * {tile};
+    const bool full = bulk && base + {tile} <= a.n;    // CTA-uniform
+    float *s = vmp_rows + buf * {n_rows * tile};
+    float qa[{per}][{dofp}];
+#pragma unroll
+    for (int r = 0; r < {per}; ++r)
+#pragma unroll
+      for (int j = 0; j < {dofp}; ++j) qa[r][j] = qn[r][j];
+    if (tile + gridDim.x < ntiles) {{
+#pragma unroll
+      for (int r = 0; r < {per}; ++r) {{
+        const long long ii = min((tile + gridDim.x) * {tile} + r * {BLOCK} + threadIdx.x, a.n - 1);
+        float *q = qn[r];
+{ld_q}
+      }}
+    }}
+    if (full) {{
+      vmp_bulk_wait_read<{max(nbuf, 1) - 1}>();   // earlier stores from this buffer have read it
+      __syncthreads();
+    }}
+#pragma unroll
+    for (int r = 0; r < {per}; ++r) {{
+      const float *q = qa[r];
+      const long long i = base + r * {BLOCK} + threadIdx.x;
+      VMP_FK_BODY
+      if (full) {{
+        const int c = r * {BLOCK} + threadIdx.x;
+{smem_rows}
+      }} else if (i < a.n) {{
+        float *o = a.out + i;
+{centre_rows}
+      }}
+    }}
+    if (full) {{
+      vmp_fence_proxy_async();
+      __syncthreads();
+      for (int r = threadIdx.x; r < {n_rows}; r += {BLOCK})
+        vmp_bulk_s2g(a.out + r * a.ldo + base, s + r * {tile}, {tile * 4});
+      vmp_bulk_commit();
+    }}
+  }}
+  vmp_bulk_wait<0>();
 }}
 """
     if not lay.has_cc:

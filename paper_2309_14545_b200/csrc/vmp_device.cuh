@@ -64,6 +64,31 @@ __device__ __forceinline__ void vmp_mbar_wait(unsigned long long *bar, unsigned 
   }
 }
 
+/* Shared -> global bulk (TMA) store of `bytes` (multiple of 16, both ends
+ * 16-byte aligned), tracked in this thread's bulk-async group. */
+__device__ __forceinline__ void vmp_bulk_s2g(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(vmp_smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void vmp_bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+/* Wait until at most N of this thread's bulk groups still read shared memory. */
+template <int N>
+__device__ __forceinline__ void vmp_bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void vmp_bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+/* Make this thread's generic-proxy shared-memory writes visible to the async
+ * (TMA) proxy before a bulk store reads them. */
+__device__ __forceinline__ void vmp_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 /* Stage the packed environment into shared memory (thread 0 issues one bulk
  * copy).  Returns the pointer kernels should read records from.  Callers must
  * vmp_mbar_wait(bar, 0) before the first dereference when staged. */
