@@ -316,6 +316,38 @@ def fkcc_summary(ctx_flush, peak: float) -> dict:
                          "frac_fp32": round(rate * f / 1e12 / peak, 4)}
         res["collision_rate"] = round(1 - float(runtime.unpack_bits(words.cpu().numpy(), n).mean()), 4)
         out[key] = res
+    out["fk_only"] = fk_only_summary(ctx_flush)
+    return out
+
+
+def fk_only_summary(ctx_flush, n: int = 1 << 22) -> dict:
+    """FK-only kernel (vmp_fk_spheres): the HBM-bound row.
+    Algorithmic bytes = joints in (4 dof) + centres out (12 per marker) per
+    configuration; peak = MEASURED_PEAKS.json hbm_gbs (copy bandwidth)."""
+    import torch
+
+    from paper_2309_14545_b200 import load_robot, runtime, workloads
+
+    hbm = float(json.loads(PEAKS.read_text()).get("hbm_gbs", 6540.0)) if PEAKS.exists() else 6540.0
+    out = {"configs": n, "peak_gbs": hbm}
+    for name in ("arm7", "baxter_standin"):
+        rob = load_robot(name)
+        q = torch.from_numpy(workloads.uniform_configs(rob.limits, n, 3)).cuda()
+        rows = 3 * len(rob.program.checks)
+        runtime.fk_spheres(rob.program, q)
+        times = []
+        for _ in range(10):
+            ctx_flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            runtime.fk_spheres(rob.program, q)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b) / 1e3)
+        t = float(np.mean(times))
+        gbs = n * 4 * (rob.tree.dof + rows) / t / 1e9
+        out[name] = {"bytes_per_config": 4 * (rob.tree.dof + rows), "us": round(t * 1e6, 1),
+                     "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
     return out
 
 

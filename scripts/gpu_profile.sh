@@ -1,19 +1,23 @@
 #!/bin/bash
 # ncu evidence: launch list of the bench + full captures of the top kernels.
+# Each capture runs only after the same command exited 0 without ncu.
 mkdir -p gpurun_out
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
 $B > gpurun_out/plain_bench.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
       --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
-for w in motion cfg3 cfg4; do
-  python scripts/profile_kernels.py $w > gpurun_out/plain_$w.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"vmp_(motion|validate)" -s 1 -c 1 \
-      -o gpurun_out/prof_$w python scripts/profile_kernels.py $w > gpurun_out/ncu_$w.log 2>&1
-done
-python scripts/profile_kernels.py cfg3 --dense > gpurun_out/plain_cfg3d.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"vmp_validate" -s 1 -c 1 \
-      -o gpurun_out/prof_cfg3_dense python scripts/profile_kernels.py cfg3 --dense > gpurun_out/ncu_cfg3d.log 2>&1
-python scripts/profile_kernels.py fk > gpurun_out/plain_fk.log 2>&1 && \
-  ncu --set full --clock-control none -k regex:"vmp_fk" -s 1 -c 1 \
-      -o gpurun_out/prof_fk python scripts/profile_kernels.py fk > gpurun_out/ncu_fk.log 2>&1
+cap() {  # cap <name> <kernel regex> <profile_kernels args...>
+  local name=$1 re=$2; shift 2
+  python scripts/profile_kernels.py "$@" > gpurun_out/plain_$name.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"$re" -s 1 -c 1 \
+      -o gpurun_out/prof_$name python scripts/profile_kernels.py "$@" > gpurun_out/ncu_$name.log 2>&1
+}
+cap motion "vmp_motion_p" motion
+cap plan "plan_cluster" motion
+cap cfg1 "vmp_validate" cfg1
+cap cfg3 "vmp_validate" cfg3
+cap cfg3_dense "vmp_validate" cfg3 --dense
+cap cfg4 "vmp_validate" cfg4
+cap fk "vmp_fk_spheres" fk
+cap knn "vmp_k_knn" knn
 ls -la gpurun_out/

@@ -1,6 +1,6 @@
 """Launch the hot kernels a few times for ncu captures (no timing printed).
 
-    python scripts/profile_kernels.py motion|cfg1|cfg3|cfg4|fk [--reps 3] [--dense]
+    python scripts/profile_kernels.py motion|cfg1|cfg3|cfg4|fk|knn [--reps 3] [--dense]
 """
 
 import argparse
@@ -29,6 +29,15 @@ def main():
         sd, gd = torch.from_numpy(mw.starts).cuda(), torch.from_numpy(mw.goals).cuda()
         for _ in range(a.reps):
             runtime.validate_motions_device(ctx.module, ctx.device_env, sd, gd, mw.resolution)
+    elif a.what == "knn":
+        import numpy as np
+        from paper_2309_14545_b200.nn import NNIndex
+        rng = np.random.default_rng(0)
+        idx = NNIndex(7)
+        idx.insert_many(rng.uniform(-1, 1, size=(100_000, 7)), range(100_000))
+        qs = rng.uniform(-1, 1, size=(4096, 7))
+        for _ in range(a.reps):
+            idx.k_nearest_many(qs, 8)
     elif a.what == "fk":
         wl = workloads.config3()
         rob = load_robot(wl.robot)
