@@ -93,3 +93,25 @@ def test_batched_prefix_queries_match_oracle(cuda, dim, n, k):
         assert got[qi, :len(ei)].tolist() == ei.tolist(), (qi, m)
         assert np.array_equal(dist[qi, :len(ei)], ed)
         assert (got[qi, len(ei):] == -1).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,k", [(7, 8), (14, 32), (2, 1)])
+def test_query_tiled_kernel_matches_oracle(cuda, dim, k):
+    """>= 2,368 queries take the CTA-tiled kernel (shared point chunks, 4
+    queries per warp, squared-distance filter); lattice points force ties."""
+    rng = np.random.default_rng(dim + 100 * k)
+    n, nq = 20_000, 3_000
+    pts = (np.round(rng.uniform(-1, 1, size=(n, dim)) * 4) / 4).astype(np.float32)
+    qs = (np.round(rng.uniform(-1, 1, size=(nq, dim)) * 4) / 4).astype(np.float32)
+    visible = rng.integers(0, n + 1, size=nq)
+    visible[:4] = (0, 1, 255, n)
+    idx = _index(pts)
+    got, dist = idx.k_nearest_many(qs, k, visible=visible)
+    soa = np.ascontiguousarray(pts.T)
+    for qi in list(range(8)) + list(rng.choice(nq, 200, replace=False)):
+        m = int(visible[qi])
+        ei, ed = O.nn_k_nearest(soa[:, :m], qs[qi], k)
+        assert got[qi, :len(ei)].tolist() == ei.tolist(), (qi, m)
+        assert np.array_equal(dist[qi, :len(ei)], ed)
+        assert (got[qi, len(ei):] == -1).all()
