@@ -8,7 +8,10 @@ Rebinds the hot-path names everywhere the reference binds them - its own
 modules import them by value at import time (planners.py:18,21,
 simplify.py:17,19, cli.py:22,24) - so the reference's
 planners, simplifier, CLI/RPC and tests run their FK, collision checks and
-motion validation on the GPU.  Host-side types (ConfigBlock, Environment,
+motion validation on the GPU; ``shortcut`` / ``bspline_smooth`` /
+``simplify_path`` and ``prm`` are replaced by their batched versions
+(simplify.py, prm.py - identical results, checked against reference runs).
+Host-side types (ConfigBlock, Environment,
 primitives, KinematicProgram) stay the reference's own; the shims duck-type
 them.  ``unpatch`` restores the originals.
 """
@@ -53,6 +56,36 @@ REPLACEMENTS = {
     "simplify_path": simplify.simplify_path,
 }
 
+#: names whose replacement is built against the patched package's own types
+ADAPTED = {"": ("prm",), "planners": ("prm",), "bench": ("prm",)}
+
+
+def reference_prm(pkg):
+    """A drop-in for the reference ``prm(problem, settings)`` (planners.py:243-291)
+    running round-batched on the device (prm.prm_rounds): same waypoints,
+    iterations and ValidationContext counters, the reference's own Path /
+    PlanResult / InvalidProblemError types."""
+    planners = importlib.import_module(f"{pkg.__name__}.planners")
+    from . import prm as batched
+
+    def prm(problem, settings=None):
+        settings = settings or planners.PlannerSettings()
+        st = batched.PRMSettings(resolution=settings.resolution,
+                                 max_iterations=settings.max_iterations, prm_k=settings.prm_k,
+                                 prm_batch=settings.prm_batch,
+                                 rake_backward=settings.rake_backward, width=settings.width)
+        try:
+            res = batched.prm_rounds(problem.robot, problem.env, problem.start, problem.goal, st)
+        except batched.InvalidProblemError as exc:
+            raise planners.InvalidProblemError(str(exc)) from None
+        path = planners.Path(list(res.waypoints)) if res.success else None
+        return planners.PlanResult(path, iterations=res.iterations,
+                                   blocks_evaluated=res.blocks_evaluated,
+                                   motion_checks=res.motion_checks)
+    prm.__doc__ = reference_prm.__doc__
+    return prm
+
+
 _SAVED: dict = {}
 #: calls routed to the B200 path per name (filled when patched with count=True)
 CALLS: dict = {}
@@ -82,7 +115,10 @@ def patch_vecmp(pkg, count: bool = False) -> list[str]:
     """
     done = []
     table = {k: (_counting(k, v) if count else v) for k, v in REPLACEMENTS.items()}
-    for sub, names in TARGETS.items():
+    adapted = reference_prm(pkg)
+    table["prm"] = _counting("prm", adapted) if count else adapted
+    targets = {sub: TARGETS.get(sub, ()) + ADAPTED.get(sub, ()) for sub in {**TARGETS, **ADAPTED}}
+    for sub, names in targets.items():
         try:
             mod = importlib.import_module(f"{pkg.__name__}.{sub}") if sub else pkg
         except ImportError:

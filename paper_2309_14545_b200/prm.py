@@ -114,12 +114,21 @@ class PRMSettings:
     width: int = 8
 
 
+class InvalidProblemError(ValueError):
+    """Start or goal rejected at setup (reference planners.py:27-28)."""
+
+
 @dataclass
 class PRMResult:
     waypoints: list | None
     iterations: int
     rounds: int
     device_calls: int
+    #: the reference's ValidationContext counters for the same run: one block
+    #: per state_valid (endpoints + samples) plus the W-lane rake blocks of
+    #: every edge; one motion check per edge (collision.py:453-465, motion.py:60)
+    blocks_evaluated: int = 0
+    motion_checks: int = 0
 
     @property
     def success(self) -> bool:
@@ -134,11 +143,11 @@ def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> 
     goal = np.asarray(goal, dtype=np.float32).reshape(-1)
     ends = ctx.validate_configs(np.stack([start, goal], axis=1))
     if not ends[0]:
-        raise ValueError("start configuration is in collision")
+        raise InvalidProblemError("start configuration is in collision")
     if not ends[1]:
-        raise ValueError("goal configuration is in collision")
+        raise InvalidProblemError("goal configuration is in collision")
     if np.array_equal(start, goal):
-        return PRMResult([start.copy(), goal.copy()], 0, 0, 1)
+        return PRMResult([start.copy(), goal.copy()], 0, 0, 1, blocks_evaluated=2)
     vertices = [start, goal]
     adjacency: list[list[tuple[int, float]]] = [[], []]
     nn = NNIndex(len(start))
@@ -146,6 +155,7 @@ def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> 
     nn.insert(goal, 1)
     draws = HaltonDraws(robot.limits)
     iterations = rounds = calls = 0
+    blocks, checks = 2, 0                  # endpoint state_valid blocks
     calls += 1
     while iterations < settings.max_iterations:
         count = min(settings.prm_batch, settings.max_iterations - iterations)
@@ -171,9 +181,12 @@ def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> 
         if edges:
             starts = np.stack([vertices[nbr] for _, nbr, _ in edges])
             goals = np.stack([vertices[vid] for vid, _, _ in edges])
-            words = validate_motions(ctx, starts, goals, settings.resolution,
-                                     backward=settings.rake_backward)     # launch 3
+            words, _, nblk = validate_motions(ctx, starts, goals, settings.resolution,  # launch 3
+                                              backward=settings.rake_backward,
+                                              width=settings.width, counts=True)
             calls += 1
+            blocks += int(nblk.sum())
+            checks += len(edges)
             free = runtime.unpack_bits(words.cpu().numpy(), len(edges))
             for (vid, nbr, dist), edge_ok in zip(edges, free):
                 if edge_ok:
@@ -181,5 +194,6 @@ def prm_rounds(robot, env, start, goal, settings: PRMSettings | None = None) -> 
                     adjacency[vid].append((nbr, dist))
         route = cheapest_route(adjacency, 0, 1)
         if route is not None:
-            return PRMResult([vertices[v] for v in route], iterations, rounds, calls)
-    return PRMResult(None, iterations, rounds, calls)
+            return PRMResult([vertices[v] for v in route], iterations, rounds, calls,
+                             blocks + iterations, checks)
+    return PRMResult(None, iterations, rounds, calls, blocks + iterations, checks)

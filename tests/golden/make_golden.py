@@ -319,6 +319,7 @@ def prm_cases() -> dict:
             out[f"settings_{key}"] = np.asarray([s.resolution, s.max_iterations, s.prm_k,
                                                  s.prm_batch, float(s.rake_backward), s.width])
             out[f"iterations_{key}"] = np.int64(res.iterations)
+            out[f"counters_{key}"] = np.asarray([res.blocks_evaluated, res.motion_checks], np.int64)
             out[f"seconds_{key}"] = np.float64(dt)
             out[f"path_{key}"] = (np.stack(res.path.waypoints) if res.success
                                   else np.zeros((0, len(case.start)), np.float32))

@@ -47,5 +47,7 @@ def test_prm_rounds_match_reference(cuda, key):
     assert out.iterations == int(FX[f"iterations_{key}"])
     assert np.array_equal(np.stack(out.waypoints), expect)
     assert out.device_calls <= 3 * out.rounds + 1
+    # the reference's ValidationContext counters for the same run
+    assert [out.blocks_evaluated, out.motion_checks] == FX[f"counters_{key}"].tolist()
     print(f"{key}: {seconds * 1e3:.1f} ms batched on the GPU vs "
           f"{float(FX[f'seconds_{key}']) * 1e3:.1f} ms reference (CPU)")

@@ -179,3 +179,15 @@ def test_gloo_two_rank_gather(n):
     for r in range(2):
         bits = np.unpackbits(results[r].view(np.uint8), bitorder="little")[:n].astype(bool)
         assert np.array_equal(bits, expect)
+
+
+def test_leading_dimension_ignores_size_one_strides():
+    """A (1, N) batch made from an (N, 1) array keeps numpy's arbitrary
+    stride for the size-1 dimension; the C ABI must get ld = N (this broke
+    1-dof robots: reference test_planners.py::TestPrm sealed pendulum)."""
+    import torch
+    from paper_2309_14545_b200.runtime import ld
+    one_row = torch.from_numpy(np.ascontiguousarray(np.zeros((64, 1), np.float32).T))
+    assert one_row.shape == (1, 64) and ld(one_row) == 64
+    assert ld(torch.zeros((3, 10))[:, :7]) == 10
+    assert ld(torch.zeros((1, 5))) == 5
