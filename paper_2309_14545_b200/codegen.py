@@ -57,7 +57,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 15
+CODEGEN_VERSION = 16
 
 
 def f32_literal(value: float) -> str:
@@ -641,7 +641,8 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     const int4 rank = __ldcg(a.order + ri);                 // (edge, n, chunks, 0)
     const long long ei = rank.x;
     const unsigned Wu = (unsigned)a.width;   // 32-bit rake index math (n < 2^31, positions
-    const unsigned first_iter = (32u * (unsigned)ci) / Wu + 1;   // < 2^31 guarded by the plan)
+    // the native width (W = 32: chunk c is iteration c + 1) skips the divisions
+    const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
     const int chunks = rank.z;
     const int failed = __ldcg(a.fail_of + ei);
     const long long n = rank.y;
@@ -652,10 +653,10 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
         s[j] = __ldg(a.starts + ei * a.sld + j);
         g[j] = __ldg(a.goals + ei * a.sld + j);
       }}
-      const unsigned S = vmp_ceil_div((unsigned)n, Wu);
+      const unsigned S = Wu == 32 ? ((unsigned)n + 31u) >> 5 : vmp_ceil_div((unsigned)n, Wu);
       const unsigned p = 32u * (unsigned)ci + lane;
-      const unsigned j = p / Wu + 1;
-      const unsigned k = p - (j - 1) * Wu;
+      const unsigned j = Wu == 32 ? (unsigned)ci + 1 : p / Wu + 1;
+      const unsigned k = Wu == 32 ? (unsigned)lane : p - (j - 1) * Wu;
       const long long idx = (long long)k * S + (a.backward ? (S - j + 1) : j);
       const bool inr = (unsigned long long)p < (unsigned long long)S * Wu && idx <= n;
       const float tt = vmp_rake_param(inr ? idx : 1, n);
@@ -665,7 +666,8 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
       if (bad && lane == 0)
-        atomicMin(a.fail_of + ei, (int)((32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1));
+        atomicMin(a.fail_of + ei, (int)(Wu == 32 ? (unsigned)ci + 1
+                                                 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1));
     }}
   }}
   if (a.fused_finalize) {{                  // the last CTA to finish writes the outputs

@@ -273,7 +273,16 @@ __device__ __forceinline__ long long vmp_discretize(const float *s, const float 
 
 /* t = f32(f64(i) / n); q = s + t (g - s), unfused (reference motion.py:69-70,
  * lanes.py:101). */
+/* t = float32(i / n) with the quotient taken in float64 (reference
+ * motion.py:69-70).  For i, n < 2^24 this equals the correctly rounded
+ * float32 quotient of the exactly representable float32 operands: double
+ * rounding can only differ at a float32 midpoint, and |i/n - M/2^e| >=
+ * 1/(n 2^e) keeps a non-midpoint quotient > 2^-49 (relative) away from every
+ * 25-bit midpoint, far outside the float64 rounding error 2^-53; an exact
+ * midpoint is representable in float64 and rounds identically.  So the cheap
+ * IEEE float32 division is bit-exact there, float64 beyond. */
 __device__ __forceinline__ float vmp_rake_param(long long i, long long n) {
+  if (n < (1ll << 24)) return __fdiv_rn((float)i, (float)n);
   return __double2float_rn(__ddiv_rn((double)i, (double)n));
 }
 

@@ -29,3 +29,13 @@ for mode in ("flush", "noflush", "flush", "noflush"):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
     print(f"{mode}: median {np.median(ts):.1f} us  min {np.min(ts):.1f} us")
+
+# precise: 200 back-to-back replays between two events (event ticks are 2 us)
+for _ in range(3):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(200):
+        mv()
+    b.record()
+    torch.cuda.synchronize()
+    print(f"200 back-to-back replays: {a.elapsed_time(b) * 1e3 / 200:.2f} us per step")
