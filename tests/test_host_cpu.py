@@ -191,3 +191,18 @@ def test_leading_dimension_ignores_size_one_strides():
     assert one_row.shape == (1, 64) and ld(one_row) == 64
     assert ld(torch.zeros((3, 10))[:, :7]) == 10
     assert ld(torch.zeros((1, 5))) == 5
+
+
+def test_rake_parameter_float32_division_equals_float64_quotient():
+    """vmp_rake_param uses the IEEE float32 quotient for n < 2^24 in place of
+    float32(i / n) taken in float64 (reference motion.py:69-70); double
+    rounding cannot differ there (csrc/vmp_device.cuh).  Exhaustive for
+    n <= 1500, 10^6 random pairs up to 2^24."""
+    for n in range(1, 1501):
+        i = np.arange(1, n + 1)
+        assert np.array_equal((i / n).astype(np.float32),
+                              i.astype(np.float32) / np.float32(n))
+    rng = np.random.default_rng(7)
+    n = rng.integers(1, 1 << 24, size=1_000_000)
+    i = (rng.random(n.size) * n).astype(np.int64) + 1
+    assert np.array_equal((i / n).astype(np.float32), i.astype(np.float32) / n.astype(np.float32))
