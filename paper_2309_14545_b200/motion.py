@@ -150,27 +150,31 @@ class MotionValidator:
 
 
 class MotionPipeline:
-    """Double-buffered stream of fixed-size edge batches from host memory.
+    """Multi-buffered stream of fixed-size edge batches from host memory.
 
     ``submit(starts, goals)`` enqueues the host->device copy of a batch on a
-    copy stream and the graph replay on the compute stream; the copy of batch
-    k+1 overlaps the rake of batch k.  ``result(ticket)`` returns that batch's
-    verdict words in pinned host memory.  Every batch still pays its own H2D
-    and D2H transfers - they are only overlapped with other batches' compute.
+    copy stream, the graph replay on the compute stream and the verdict
+    read-back on a third stream, so batch k+1's H2D and batch k-1's D2H
+    overlap batch k's rake and the compute stream only ever runs rakes.
+    ``result(ticket)`` returns that batch's verdict words in pinned host
+    memory.  Every batch still pays its own H2D and D2H transfers - they are
+    only overlapped with other batches' compute.  Keep up to ``depth - 1``
+    batches in flight before asking for results.
     """
 
     def __init__(self, ctx: ValidationContext, n_edges: int, resolution: float, *,
-                 width: int = 32, depth: int = 2):
+                 width: int = 32, depth: int = 3):
         torch = runtime.require_cuda()
         self.torch = torch
         self.slots = [MotionValidator(ctx, n_edges, resolution, width=width) for _ in range(depth)]
         self.copy_stream = torch.cuda.Stream()
+        self.d2h_stream = torch.cuda.Stream()
         self.compute_stream = torch.cuda.current_stream()
         self.host = [torch.empty(s.bits.shape, dtype=torch.int32).pin_memory() for s in self.slots]
         self.copied = [torch.cuda.Event() for _ in self.slots]
+        self.raked = [torch.cuda.Event() for _ in self.slots]
         self.done = [torch.cuda.Event() for _ in self.slots]
-        self.freed = [torch.cuda.Event() for _ in self.slots]
-        for ev in self.freed:
+        for ev in self.raked + self.done:
             ev.record(self.compute_stream)
         self.count = 0
 
@@ -178,15 +182,18 @@ class MotionPipeline:
         k = self.count % len(self.slots)
         slot = self.slots[k]
         with self.torch.cuda.stream(self.copy_stream):
-            self.copy_stream.wait_event(self.freed[k])          # slot's previous rake finished
+            self.copy_stream.wait_event(self.raked[k])          # slot's previous rake read its edges
             slot.starts.copy_(runtime._as_tensor(starts), non_blocking=True)
             slot.goals.copy_(runtime._as_tensor(goals), non_blocking=True)
             self.copied[k].record(self.copy_stream)
         self.compute_stream.wait_event(self.copied[k])
+        self.compute_stream.wait_event(self.done[k])            # previous verdicts read back
         slot()                                                  # graph replay on compute stream
-        self.freed[k].record(self.compute_stream)
-        self.host[k].copy_(slot.bits, non_blocking=True)
-        self.done[k].record(self.compute_stream)
+        self.raked[k].record(self.compute_stream)
+        with self.torch.cuda.stream(self.d2h_stream):
+            self.d2h_stream.wait_event(self.raked[k])
+            self.host[k].copy_(slot.bits, non_blocking=True)
+            self.done[k].record(self.d2h_stream)
         self.count += 1
         return self.count - 1
 

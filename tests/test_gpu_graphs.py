@@ -48,14 +48,18 @@ def test_motion_pipeline_overlapped_batches(cuda):
                         torch.from_numpy(mw.goals[idx]).pin_memory()))
     expect = [runtime.unpack_bits(M.validate_motions(ctx, s, g, mw.resolution).cpu().numpy(), E)
               for s, g in batches]
-    pipe = M.MotionPipeline(ctx, E, mw.resolution)
-    prev = None
-    for k, (s, g) in enumerate(batches):
-        t = pipe.submit(s, g)
-        if prev is not None:
-            assert runtime.unpack_bits(pipe.result(prev), E).tolist() == expect[k - 1].tolist()
-        prev = t
-    assert runtime.unpack_bits(pipe.result(prev), E).tolist() == expect[-1].tolist()
+    for depth in (2, 3):
+        pipe = M.MotionPipeline(ctx, E, mw.resolution, depth=depth)
+        inflight = []
+        for k, (s, g) in enumerate(batches + batches):        # slots are reused
+            inflight.append((k, pipe.submit(s, g)))
+            if len(inflight) == depth:
+                j, t = inflight.pop(0)
+                got = runtime.unpack_bits(pipe.result(t), E)
+                assert got.tolist() == expect[j % len(batches)].tolist()
+        for j, t in inflight:
+            assert runtime.unpack_bits(pipe.result(t), E).tolist() == \
+                expect[j % len(batches)].tolist()
 
 
 @pytest.mark.parametrize("early", [True, False])
