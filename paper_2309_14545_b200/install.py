@@ -9,8 +9,9 @@ modules import them by value at import time (planners.py:18,21,
 simplify.py:17,19, cli.py:22,24) - so the reference's
 planners, simplifier, CLI/RPC and tests run their FK, collision checks and
 motion validation on the GPU; ``shortcut`` / ``bspline_smooth`` /
-``simplify_path`` and ``prm`` are replaced by their batched versions
-(simplify.py, prm.py - identical results, checked against reference runs).
+``simplify_path``, ``prm`` and ``rrt_connect`` are replaced by their batched
+versions (simplify.py, prm.py, rrt.py - identical results, checked against
+reference runs).
 Host-side types (ConfigBlock, Environment,
 primitives, KinematicProgram) stay the reference's own; the shims duck-type
 them.  ``unpatch`` restores the originals.
@@ -57,7 +58,8 @@ REPLACEMENTS = {
 }
 
 #: names whose replacement is built against the patched package's own types
-ADAPTED = {"": ("prm",), "planners": ("prm",), "bench": ("prm",)}
+ADAPTED = {"": ("prm", "rrt_connect"), "planners": ("prm", "rrt_connect"),
+           "bench": ("prm", "rrt_connect")}
 
 
 def reference_prm(pkg):
@@ -84,6 +86,32 @@ def reference_prm(pkg):
                                    motion_checks=res.motion_checks)
     prm.__doc__ = reference_prm.__doc__
     return prm
+
+
+def reference_rrt_connect(pkg):
+    """A drop-in for the reference ``rrt_connect(problem, settings)``
+    (planners.py:180-210) with batched connect chains (rrt.rrt_connect_batched):
+    same waypoints, iterations and counters, the reference's own types."""
+    planners = importlib.import_module(f"{pkg.__name__}.planners")
+    from . import prm as batched_prm
+    from . import rrt as batched
+
+    def rrt_connect(problem, settings=None):
+        settings = settings or planners.PlannerSettings()
+        st = batched.RRTSettings(resolution=settings.resolution, range=settings.range,
+                                 max_iterations=settings.max_iterations,
+                                 rake_backward=settings.rake_backward, width=settings.width)
+        try:
+            res = batched.rrt_connect_batched(problem.robot, problem.env, problem.start,
+                                              problem.goal, st)
+        except batched_prm.InvalidProblemError as exc:
+            raise planners.InvalidProblemError(str(exc)) from None
+        path = planners.Path(list(res.waypoints)) if res.success else None
+        return planners.PlanResult(path, iterations=res.iterations,
+                                   blocks_evaluated=res.blocks_evaluated,
+                                   motion_checks=res.motion_checks)
+    rrt_connect.__doc__ = reference_rrt_connect.__doc__
+    return rrt_connect
 
 
 _SAVED: dict = {}
@@ -115,8 +143,9 @@ def patch_vecmp(pkg, count: bool = False) -> list[str]:
     """
     done = []
     table = {k: (_counting(k, v) if count else v) for k, v in REPLACEMENTS.items()}
-    adapted = reference_prm(pkg)
-    table["prm"] = _counting("prm", adapted) if count else adapted
+    for name, make in (("prm", reference_prm), ("rrt_connect", reference_rrt_connect)):
+        adapted = make(pkg)
+        table[name] = _counting(name, adapted) if count else adapted
     targets = {sub: TARGETS.get(sub, ()) + ADAPTED.get(sub, ()) for sub in {**TARGETS, **ADAPTED}}
     for sub, names in targets.items():
         try:

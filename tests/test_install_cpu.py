@@ -31,7 +31,7 @@ def test_patch_rebinds_all_import_sites(vecmp_pkg):
     from paper_2309_14545_b200 import collision, install, motion, program
     from paper_2309_14545_b200 import simplify as batched
     done = install.patch_vecmp(vecmp_pkg)
-    assert len(done) == 37
+    assert len(done) == 40
     planners = importlib.import_module("vecmp.planners")
     simplify = importlib.import_module("vecmp.simplify")
     cli = importlib.import_module("vecmp.cli")
@@ -43,6 +43,8 @@ def test_patch_rebinds_all_import_sites(vecmp_pkg):
     assert importlib.import_module("vecmp.bench").simplify_path is batched.simplify_path
     assert vecmp_pkg.shortcut is batched.shortcut and simplify.bspline_smooth is batched.bspline_smooth
     assert vecmp_pkg.prm is planners.prm and "round-batched" in planners.prm.__doc__
+    assert vecmp_pkg.rrt_connect is planners.rrt_connect
+    assert "batched connect" in planners.rrt_connect.__doc__
     assert vecmp_pkg.program.evaluate_program is program.evaluate_program
     assert vecmp_pkg.collision.validate_block is collision.validate_block
     install.unpatch_vecmp(vecmp_pkg)
