@@ -1,6 +1,6 @@
 """Launch the hot kernels a few times for ncu captures (no timing printed).
 
-    python scripts/profile_kernels.py motion|cfg1|cfg3|cfg4|fk|knn [--reps 3] [--dense]
+    python scripts/profile_kernels.py motion|cfg1|cfg3|cfg4|cfg5_<P>|fk|knn [--reps 3] [--dense] [--n N]
 """
 
 import argparse
@@ -20,6 +20,7 @@ def main():
     p.add_argument("what")
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--dense", action="store_true")
+    p.add_argument("--n", type=int, default=1 << 20)
     a = p.parse_args()
     torch.cuda.set_device(0)
     if a.what == "motion":
@@ -45,7 +46,11 @@ def main():
         for _ in range(a.reps):
             runtime.fk_spheres(rob.program, q)
     else:
-        wl = {"cfg1": workloads.config1, "cfg3": workloads.config3, "cfg4": workloads.config4}[a.what]()
+        if a.what.startswith("cfg5_"):
+            wl = workloads.config5(a.n, int(a.what[5:]))
+        else:
+            wl = {"cfg1": workloads.config1, "cfg3": workloads.config3,
+                  "cfg4": workloads.config4}[a.what]()
         rob = load_robot(wl.robot)
         ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
         q = torch.from_numpy(wl.q).cuda()
