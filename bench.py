@@ -253,8 +253,9 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                    "mean_states_per_edge": round(float(n_np.mean()), 2),
                    "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
                    "launch": "CUDA graph (plan + rake, PDL edge) via motion.MotionValidator; "
-                             "e2e through motion.MotionPipeline (3 slots: H2D of step k+1 and "
-                             "D2H of step k-1 overlap the rake of step k)",
+                             "e2e through motion.MotionPipeline (3 slots, a compute stream "
+                             "each: H2D of step k+1, D2H of step k-1 and the neighbouring rakes "
+                             "overlap the rake of step k)",
                    "parallelism": f"dp{world} (independent edges per rank)"},
         "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4),

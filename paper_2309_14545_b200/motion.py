@@ -153,9 +153,11 @@ class MotionPipeline:
     """Multi-buffered stream of fixed-size edge batches from host memory.
 
     ``submit(starts, goals)`` enqueues the host->device copy of a batch on a
-    copy stream, the graph replay on the compute stream and the verdict
-    read-back on a third stream, so batch k+1's H2D and batch k-1's D2H
-    overlap batch k's rake and the compute stream only ever runs rakes.
+    copy stream, the graph replay on its slot's own compute stream and the
+    verdict read-back on a read-back stream: batch k+1's H2D and batch k-1's
+    D2H overlap batch k's rake, and consecutive rakes may overlap each other
+    (the next batch's plan and first work items fill the previous rake's
+    drain).
     ``result(ticket)`` returns that batch's verdict words in pinned host
     memory.  Every batch still pays its own H2D and D2H transfers - they are
     only overlapped with other batches' compute.  Keep up to ``depth - 1``
@@ -169,13 +171,14 @@ class MotionPipeline:
         self.slots = [MotionValidator(ctx, n_edges, resolution, width=width) for _ in range(depth)]
         self.copy_stream = torch.cuda.Stream()
         self.d2h_stream = torch.cuda.Stream()
-        self.compute_stream = torch.cuda.current_stream()
+        self.compute_streams = [torch.cuda.Stream() for _ in self.slots]
+        origin = torch.cuda.current_stream()
         self.host = [torch.empty(s.bits.shape, dtype=torch.int32).pin_memory() for s in self.slots]
         self.copied = [torch.cuda.Event() for _ in self.slots]
         self.raked = [torch.cuda.Event() for _ in self.slots]
         self.done = [torch.cuda.Event() for _ in self.slots]
         for ev in self.raked + self.done:
-            ev.record(self.compute_stream)
+            ev.record(origin)
         self.count = 0
 
     def submit(self, starts, goals) -> int:
@@ -186,10 +189,12 @@ class MotionPipeline:
             slot.starts.copy_(runtime._as_tensor(starts), non_blocking=True)
             slot.goals.copy_(runtime._as_tensor(goals), non_blocking=True)
             self.copied[k].record(self.copy_stream)
-        self.compute_stream.wait_event(self.copied[k])
-        self.compute_stream.wait_event(self.done[k])            # previous verdicts read back
-        slot()                                                  # graph replay on compute stream
-        self.raked[k].record(self.compute_stream)
+        cs = self.compute_streams[k]
+        cs.wait_event(self.copied[k])
+        cs.wait_event(self.done[k])                             # previous verdicts read back
+        with self.torch.cuda.stream(cs):
+            slot()                                              # graph replay on the slot's stream
+        self.raked[k].record(cs)
         with self.torch.cuda.stream(self.d2h_stream):
             self.d2h_stream.wait_event(self.raked[k])
             self.host[k].copy_(slot.bits, non_blocking=True)
