@@ -159,6 +159,12 @@ int vmp_nn_distances(const float *points, int64_t n_points, int64_t ld, int32_t 
                      const float *queries, int64_t n_queries, int64_t qld, float *out, int64_t ldo,
                      void *stream);
 
+/* Debug: copy up to n words of the rake kernel's timeline (recorded only when
+ * the process starts with VMP_MOTION_TRACE set; 8 words per CTA of the last
+ * launch: entry, plan ready, warp 0-3 queue empty, exit - globaltimer ns -
+ * and work items taken).  Returns the words copied, 0 when tracing is off. */
+int64_t vmp_debug_motion_trace(uint64_t *host, int64_t n);
+
 /* Select the CUDA device used by subsequent vmp calls on this thread (robots
  * and environments remember the device they were created on). */
 int vmp_set_device(int32_t device);

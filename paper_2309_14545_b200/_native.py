@@ -43,7 +43,7 @@ EXPORTS = (
     "vmp_env_create", "vmp_env_destroy", "vmp_env_bytes", "vmp_fk_rows", "vmp_fk_spheres",
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
-    "vmp_knn", "vmp_nn_distances",
+    "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace",
 )
 VMP_KNN_MAX_K = 32
 VMP_KNN_MAX_DIM = 64
@@ -114,6 +114,7 @@ def lib() -> ctypes.CDLL:
                     ctypes.c_int),
         "vmp_nn_distances": ([vp, c_i64, c_i64, c_i32, vp, c_i64, c_i64, vp, c_i64, vp],
                              ctypes.c_int),
+        "vmp_debug_motion_trace": ([vp, c_i64], c_i64),
         "vmp_set_device": ([c_i32], ctypes.c_int),
         "vmp_device_info": ([ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)], ctypes.c_int),
     }

@@ -40,6 +40,7 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
 SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
+MOTION_MIN_CTAS = 5     # occupancy target of the register-capped rake variant
 FK_SMEM_TILE = 160 * 1024   # largest vmp_fk_spheres centre tile (shared memory bytes)
 
 
@@ -57,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 16
+CODEGEN_VERSION = 19
 
 
 def f32_literal(value: float) -> str:
@@ -574,14 +575,24 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
 template <int PRUNE, int STOP, bool STAGED>
 __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // Work items are (chunk c, edge e) pairs enumerated round by round (c-major,
-  // dense: the plan kernels sort edges by chunk count so round c lists exactly
-  // the edges that have a chunk c).  Chunk c is rake positions [32c, 32c + 32)
-  // of the W-lane rake sequence - exactly one rake iteration when W = 32.
-  // One item per atomic keeps the work granularity at one warp-chunk, so the
-  // tail is one chunk long instead of a whole edge; items of edges already
-  // known to fail at an earlier iteration are skipped.
+  // dense).  Chunk c is rake positions [32c, 32c + 32) of the W-lane rake
+  // sequence - exactly one rake iteration when W = 32.  Round 0 holds every
+  // edge, in input order, and needs nothing from the plan: its items compute
+  // their edge's discretisation themselves and run while the plan kernel
+  // (programmatic dependent launch) sorts the edges by chunk count for rounds
+  // >= 1; a warp waits for the plan only when it first reaches round 1.  One
+  // item per atomic keeps the work granularity at one warp-chunk; items of
+  // edges already known to fail at an earlier iteration are skipped.  The
+  // finalize kernel (programmatic dependent launch) writes the outputs.
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
+  __shared__ long long vmp_off[{BLOCK} / 32][VMP_OFF_CACHE];   // per-warp round offsets
+  // debug timeline (a.trace, VMP_MOTION_TRACE): 8 words per CTA
+  unsigned long long *trace = a.trace ? a.trace + 8 * blockIdx.x : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = vmp_gtime();
+  // the finalize kernel may launch now: its CTAs fill SM slots as rake CTAs
+  // retire and wait (griddepcontrol.wait) for this whole grid
+  asm volatile("griddepcontrol.launch_dependents;");
   const float4 *env = a.env.rec;
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
@@ -590,19 +601,16 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     env = vmp_smem;
   }}
   const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
-  const int lane = threadIdx.x & 31;
-  // programmatic dependent launch: everything above (env staging, const check)
-  // overlapped the plan kernel; wait for its results here
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // plan data was written while this grid was already running: read it through
-  // L2 (ld.global.cg), never the non-coherent path; round offsets go to smem
-  const long long total_items = (long long)__ldcg(&a.hdr->total_items);
-  const long long split = __ldcg(a.off + (VMP_HBINS - 1));
-  const long long n_big = __ldcg(&a.hdr->n_big);
-  __shared__ long long vmp_off[VMP_HBINS];
-  const int n_off = (int)min(__ldcg(&a.hdr->max_chunks) + 1u, (unsigned)VMP_HBINS);
-  for (int i = threadIdx.x; i < n_off; i += blockDim.x) vmp_off[i] = __ldcg(a.off + i);
-  __syncthreads();
+  if (trace && threadIdx.x == 0) trace[1] = vmp_gtime();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long E = a.n_edges;
+  const unsigned Wu = (unsigned)a.width;   // 32-bit rake index math (n < 2^31, positions
+                                           // < 2^31 guarded by the plan)
+  // until the plan is read, only round 0 (items t < E) is known to exist
+  long long total_items = E, split = 0, n_big = 0;
+  int n_off = 0;
+  bool planned = false;
+  unsigned taken = 0;
   // striped work queue: stripe s serves items t = VMP_QSTRIPES * i + s; a warp
   // starts on its own stripe and moves on when it runs dry
   const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
@@ -617,36 +625,65 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
     const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
     have = false;
+    if (t >= total_items && !planned) {{     // first item past round 0: read the plan
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      // plan data was written while this grid was already running: read it
+      // through L2 (ld.global.cg), never the non-coherent path
+      total_items = (long long)__ldcg(&a.hdr->total_items);
+      split = __ldcg(a.off + (VMP_HBINS - 1));
+      n_big = __ldcg(&a.hdr->n_big);
+      n_off = (int)min(__ldcg(&a.hdr->max_chunks) + 1u, (unsigned)VMP_HBINS);
+      for (int i = lane; i < min(n_off, VMP_OFF_CACHE); i += 32) vmp_off[warp][i] = __ldcg(a.off + i);
+      __syncwarp();
+      planned = true;
+    }}
     if (t >= total_items) {{                // stripe dry: look at all stripes at once
       const unsigned long long seen = lane < VMP_QSTRIPES ? __ldcg(&a.hdr->counter[16 * lane]) : 0;
       const unsigned open = __ballot_sync(VMP_FULL, lane < VMP_QSTRIPES &&
                                           (long long)seen * VMP_QSTRIPES + lane < total_items);
-      if (!open || ++dry > 4 * VMP_QSTRIPES) break;
+      if (!open || ++dry > 4 * VMP_QSTRIPES) {{
+        if (trace && lane == 0) {{
+          trace[2 + warp] = vmp_gtime();
+          atomicAdd(trace + 7, (unsigned long long)taken);
+        }}
+        break;
+      }}
       stripe = __ffs(open) - 1;
       continue;
     }}
+    ++taken;
     if (t + guard < total_items) {{
       if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
       have = true;
     }}
-    long long ci, ri;
-    if (t < split) {{
-      ci = vmp_find_round(vmp_off, n_off, t, lane);
-      ri = t - vmp_off[ci];
-    }} else {{                              // rounds beyond the histogram (very long edges)
-      const long long u = t - split;
-      ci = (VMP_HBINS - 1) + u / n_big;
-      ri = u - (ci - (VMP_HBINS - 1)) * n_big;
+    long long ci, ei;
+    int n, chunks;
+    if (t < E) {{                            // round 0: edge t, discretised here
+      ci = 0;
+      ei = t;
+      n = vmp_discretize_edge<{lay.dof}>(a.starts + ei * a.sld, a.goals + ei * a.sld, a.resolution);
+      chunks = (int)vmp_rake_chunks((unsigned)n, Wu);
+      if (lane == 0) a.n_of[ei] = n;        // for the finalize kernel
+    }} else {{
+      long long ri;
+      if (t < split) {{
+        ci = vmp_find_round_any(vmp_off[warp], a.off, n_off, t, lane);
+        ri = t - (ci < VMP_OFF_CACHE ? vmp_off[warp][ci] : __ldcg(a.off + ci));
+      }} else {{                            // rounds beyond the histogram (very long edges)
+        const long long u = t - split;
+        ci = (VMP_HBINS - 1) + u / n_big;
+        ri = u - (ci - (VMP_HBINS - 1)) * n_big;
+      }}
+      const int4 rank = __ldcg(a.order + ri);               // (edge, n, chunks, 0)
+      ei = rank.x;
+      n = rank.y;
+      chunks = rank.z;
     }}
-    const int4 rank = __ldcg(a.order + ri);                 // (edge, n, chunks, 0)
-    const long long ei = rank.x;
-    const unsigned Wu = (unsigned)a.width;   // 32-bit rake index math (n < 2^31, positions
+    if (ci >= chunks) continue;             // absent (only past the histogram)
     // the native width (W = 32: chunk c is iteration c + 1) skips the divisions
     const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
-    const int chunks = rank.z;
-    const int failed = __ldcg(a.fail_of + ei);
-    const long long n = rank.y;
-    if (ci < chunks && failed > (int)first_iter) {{   // else: absent, or cannot lower the count
+    const int fe = __ldcg(a.fail_enc + ei);  // 0, or INT_MAX - first failing iteration
+    if (fe == 0 || 0x7fffffff - fe > (int)first_iter) {{   // else: cannot lower the count
       float s[{dofp}], g[{dofp}];
 #pragma unroll
       for (int j = 0; j < {lay.dof}; ++j) {{
@@ -665,33 +702,14 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
       const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
-      if (bad && lane == 0)
-        atomicMin(a.fail_of + ei, (int)(Wu == 32 ? (unsigned)ci + 1
-                                                 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1));
-    }}
-  }}
-  if (a.fused_finalize) {{                  // the last CTA to finish writes the outputs
-    __shared__ unsigned vmp_last;
-    __threadfence();                        // publish this warp's fail_of updates device-wide
-    __syncthreads();
-    if (threadIdx.x == 0) {{
-      __threadfence();
-      vmp_last = atomicAdd(&a.hdr->done_ctas, 1u) == gridDim.x - 1;
-    }}
-    __syncthreads();
-    if (vmp_last) {{
-      __threadfence();
-      vmp_motion_outputs(a.n_edges, a.width, a.n_of, a.fail_of, a.bits, a.n_states, a.blocks,
-                         0, {BLOCK}, threadIdx.x);
-      // leave the workspace header zeroed for the next call (no memset launch)
-      for (int s = threadIdx.x; s < VMP_QSTRIPES; s += {BLOCK}) a.hdr->counter[16 * s] = 0;
-      if (threadIdx.x == 0) {{
-        a.hdr->max_chunks = 0;
-        a.hdr->done_ctas = 0;
-        a.hdr->plan_done = 0;
+      if (bad && lane == 0) {{
+        const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
+        atomicMax(a.fail_enc + ei, 0x7fffffff - (int)it);
       }}
     }}
+
   }}
+  if (trace && threadIdx.x == 0) trace[6] = vmp_gtime();
 }}
 """
     for prune in (0, 1):
@@ -714,6 +732,12 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                         f'vmp_motion_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '
                         f'{{ vmp_motion_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
+            if staged:
+                # the hot rake variant, register-capped for MOTION_MIN_CTAS CTAs per
+                # SM; the host uses it only when it compiled without local memory
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
+                        f'vmp_motion_p{prune}_s2_g1_o(VmpMotionArgs a) '
+                        f'{{ vmp_motion_body<{prune}, 2, true>(a); }}\n')
     return src
 
 

@@ -27,17 +27,22 @@ typedef struct {
   int pad_;
 } VmpValidateArgs;
 
-/* Motion workspace (all zero-initialised by one memset, then the plan):
+/* Motion workspace (zero-filled once by the caller; every call leaves it zero):
  *   VmpMotionHeader
  *   unsigned hist[VMP_HBINS], fill[VMP_HBINS]   chunk-count histogram / scatter cursors
  *   long long off[VMP_HBINS]                    first work item of chunk round c
- *   int n[E], chunks[E], fail[E]                per-edge plan
+ *   int fail_enc[E]                             per edge: INT_MAX - first failing
+ *                                               iteration, 0 while none
+ *   int n[E], chunks[E]                         per edge: discretisation count (rake
+ *                                               round 0); chunks (multi-kernel plan)
  *   int4 order[E]                               (edge, n, chunks, 0) by chunk count desc
- * Work item t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c,
- * where off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest
- * edges (chunks >= HBINS-1) and skip absent chunks. */
+ * Work item t < E is round 0 of edge t (input order, no plan needed); item
+ * E <= t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c, where
+ * off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest edges
+ * (chunks >= HBINS-1) and skip absent chunks. */
 #define VMP_HBINS 1024
 #define VMP_QSTRIPES 16           /* item queue striped over 16 counters (t % 16) */
+#define VMP_OFF_CACHE 64          /* round offsets a rake warp keeps in shared memory */
 typedef struct {
   unsigned long long counter[VMP_QSTRIPES * 16]; /* stripe s at [16 s]: one 128 B line each */
   unsigned long long total_items; /* written by the scan kernel */
@@ -57,17 +62,16 @@ typedef struct {
   VmpEnvView env;
   VmpMotionHeader *hdr;
   const long long *off; /* first work item of each chunk round */
-  const int *n_of;      /* discretisation count per edge (plan kernel) */
-  const int *chunks_of; /* 32-position chunks per edge (plan kernel) */
-  int *fail_of;         /* first failing rake iteration, INT_MAX while none */
   const int4 *order;    /* rank records (edge, n, chunks, 0), chunk count descending */
-  unsigned int *bits;   /* outputs, written by the last CTA when fused_finalize */
-  int *n_states;
-  int *blocks;
+  int *fail_enc;        /* per edge: INT_MAX - first failing iteration, 0 while none */
+  int *n_of;            /* per edge: discretisation count (written by round 0) */
+  unsigned long long *trace; /* debug timeline (VMP_MOTION_TRACE), normally null:
+                                per CTA [entry, plan ready, warp 0-3 queue empty,
+                                exit, work items taken] in globaltimer ns */
   int width;            /* rake lane width W whose block counts are reproduced */
   int backward;         /* comb strata top-down */
   int stage;
-  int fused_finalize;   /* 1: the last CTA to finish writes the outputs */
+  int pad_;
 } VmpMotionArgs;
 
 typedef struct {

@@ -27,6 +27,13 @@ __device__ __forceinline__ void vmp_sincos(float x, float *s, float *c) {
   __sincosf(r, s, c);
 }
 
+/* Nanosecond global timer (debug timelines only). */
+__device__ __forceinline__ unsigned long long vmp_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 /* ---------------------------------------------------------------- staging */
 
 __device__ __forceinline__ unsigned vmp_smem_addr(const void *p) {
@@ -267,8 +274,20 @@ template <int D>
 __device__ __forceinline__ long long vmp_discretize(const float *s, const float *g, double res) {
   float dist = __fsqrt_rn(vmp_np_sumsq<D>(s, g));
   double steps = ceil(__ddiv_rn((double)dist, res));
-  long long n = (long long)steps;
-  return n < 1 ? 1 : n;
+  long long n = steps < 1.0 ? 1 : (long long)steps;
+  return n > 0x7fffffffLL ? 0x7fffffffLL : n;     /* same clamp as the plan kernels */
+}
+
+/* Discretisation count of the edge whose start / goal rows are at s / g. */
+template <int D>
+__device__ __noinline__ int vmp_discretize_edge(const float *s, const float *g, double res) {
+  float sv[D > 0 ? D : 1], gv[D > 0 ? D : 1];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    sv[j] = __ldg(s + j);
+    gv[j] = __ldg(g + j);
+  }
+  return (int)vmp_discretize<D>(sv, gv, res);
 }
 
 /* t = f32(f64(i) / n); q = s + t (g - s), unfused (reference motion.py:69-70,
@@ -290,6 +309,31 @@ __device__ __forceinline__ float vmp_lerp_exact(float s, float g, float t) {
   return __fadd_rn(s, __fmul_rn(t, __fsub_rn(g, s)));
 }
 
+/* Outputs of edges [tid0 + tid, ...) stepping by nthreads (whole warps):
+ * verdict word by ballot, n and the W-lane rake block count; resets each
+ * edge's failure record (INT_MAX - first failing iteration, 0 = none) for the
+ * next call. */
+__device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w);
+__device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width, const int *n_of,
+                                                   int *fail_enc, unsigned *bits, int *n_states,
+                                                   int *blocks, long long tid0, long long nthreads,
+                                                   int tid) {
+  for (long long base = tid0; base < n_edges; base += nthreads) {
+    const long long e = base + tid;
+    const bool inr = e < n_edges;
+    const int fe = inr ? __ldcg(fail_enc + e) : 0;
+    const bool ok = inr && fe == 0;
+    const unsigned m = __ballot_sync(VMP_FULL, ok);
+    if (inr) {
+      if (fe) fail_enc[e] = 0;
+      if ((tid & 31) == 0) bits[e >> 5] = m;
+      const int n = __ldcg(n_of + e);
+      if (n_states) n_states[e] = n;
+      if (blocks) blocks[e] = ok ? (int)vmp_ceil_div((unsigned)n, (unsigned)width) : 0x7fffffff - fe;
+    }
+  }
+}
+
 /* ceil(n / w) and the number of 32-position chunks of a W-lane rake over n
  * states, with 32-bit division (n < 2^31, w >= 1). */
 __device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w) {
@@ -299,25 +343,19 @@ __device__ __forceinline__ unsigned vmp_rake_chunks(unsigned n, unsigned w) {
   return (unsigned)(((unsigned long long)vmp_ceil_div(n, w) * w + 31ull) >> 5);
 }
 
-/* Motion outputs from the per-edge plan: verdict bit (no failure recorded),
- * n, and the W-rake block count (failing iteration, or S = ceil(n / W)).
- * Threads [tid0, tid0 + nthreads) of a group; nthreads a multiple of 32. */
-__device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width, const int *n_of,
-                                                   const int *fail_of, unsigned *bits,
-                                                   int *n_states, int *blocks, long long tid0,
-                                                   long long nthreads, int tid) {
-  for (long long base = tid0; base < n_edges; base += nthreads) {
-    const long long e = base + tid;
-    const bool inr = e < n_edges;
-    const int fail = inr ? __ldcg(fail_of + e) : 0;
-    const bool ok = inr && fail == 0x7fffffff;
-    const unsigned m = __ballot_sync(VMP_FULL, ok);
-    if (inr) {
-      if ((tid & 31) == 0) bits[e >> 5] = m;
-      const long long n = __ldcg(n_of + e);
-      if (n_states) n_states[e] = (int)n;
-      if (blocks) blocks[e] = ok ? (int)vmp_ceil_div((unsigned)n, (unsigned)width) : fail;
-    }
+
+
+/* Same, with the first VMP_OFF_CACHE offsets in shared memory and the rest
+ * read through L2. */
+__device__ __forceinline__ int vmp_find_round_any(const long long *off_s, const long long *off_g,
+                                                  int n_off, long long t, int lane) {
+  int base = 0;
+  for (;;) {
+    const int c = base + lane;
+    const bool le = c < n_off && (c < VMP_OFF_CACHE ? off_s[c] : __ldcg(off_g + c)) <= t;
+    const unsigned m = __ballot_sync(VMP_FULL, le);
+    if (m != VMP_FULL || base + 32 >= VMP_HBINS) return base + 31 - __clz(m);
+    base += 32;
   }
 }
 
