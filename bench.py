@@ -252,7 +252,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                    "valid_edge_fraction": round(float(valid.mean()), 4),
                    "mean_states_per_edge": round(float(n_np.mean()), 2),
                    "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
-                   "launch": "CUDA graph (plan + rake, PDL edge) via motion.MotionValidator; "
+                   "launch": "CUDA graph (plan -> rake -> finalize, PDL edges) via motion.MotionValidator; "
                              "e2e through motion.MotionPipeline (3 slots, a compute stream "
                              "each: H2D of step k+1, D2H of step k-1 and the neighbouring rakes "
                              "overlap the rake of step k)",
@@ -266,7 +266,8 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                      "note": "states fully evaluated by the rake (valid edges: all n; invalid: "
                              "iterations before the failing one) x reference dense flop/state; "
                              "peak: " + peak_src},
-        "gpu_launches": 2 * args.steps,                   # plan + rake kernel per step
+        # per step (one graph replay): cluster plan + rake + finalize kernels
+        "gpu_launches": 3 * args.steps,
         "e2e": {"value": round(e2e_value, 1), "unit": "edges/s",
                 "h2d_bytes_per_step": int(mw.starts.nbytes + mw.goals.nbytes),
                 "d2h_bytes_per_step": int(bits.numel() * 4)},
