@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 19
+CODEGEN_VERSION = 20
 
 
 def f32_literal(value: float) -> str:
@@ -358,11 +358,13 @@ def _state_function(lay: RobotLayout) -> str:
         emit(f"        const float4 *pp = p + j * split * {f4};")
         emit(f"        const float4 bnd = pp[{bound}];")
         emit(f"        const float brad = {radius};")
-        emit("        bool nr = false;")
+        # one compare per obstacle: the minimum over the groups of the expanded
+        # bound distance (near iff some group's is <= the threshold)
         for gi, grp in enumerate(groups):
             mx, my, mz = _xyz(grp[len(grp) // 2])
-            emit(f"        nr |= !vmp_clear_sphere({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad);")
-        emit("        near |= (unsigned)nr << j;")
+            w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
+            emit(f"        float wm{gi} = {w};" if gi == 0 else f"        wm0 = fminf(wm0, {w});")
+        emit("        near |= (unsigned)(wm0 <= bnd.w) << j;" if groups else "")
         emit("      }")
         emit("      unsigned todo = __reduce_or_sync(VMP_FULL, near);")
         emit("      while (todo) {")
@@ -622,6 +624,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   unsigned long long grab = 0;
   bool have = false;
   for (;;) {{
+    const unsigned long long t_top = trace ? vmp_gtime() : 0;
     if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
     const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
     have = false;
@@ -683,6 +686,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     // the native width (W = 32: chunk c is iteration c + 1) skips the divisions
     const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
     const int fe = __ldcg(a.fail_enc + ei);  // 0, or INT_MAX - first failing iteration
+    const unsigned long long t_start = trace ? vmp_gtime() : 0;
     if (fe == 0 || 0x7fffffff - fe > (int)first_iter) {{   // else: cannot lower the count
       float s[{dofp}], g[{dofp}];
 #pragma unroll
@@ -706,6 +710,13 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
         const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
         atomicMax(a.fail_enc + ei, 0x7fffffff - (int)it);
       }}
+    }}
+    if (trace && lane == 0 && t < VMP_TRACE_ITEMS) {{   // per item: start, end, round | edge, warp | top
+      unsigned long long *rec = a.trace + VMP_TRACE_ITEM0 + 4 * t;
+      rec[0] = t_start;
+      rec[1] = vmp_gtime();
+      rec[2] = ((unsigned long long)ci << 32) | (unsigned long long)ei;
+      rec[3] = ((unsigned long long)wid << 48) | (t_top & 0xffffffffffffull);
     }}
 
   }}

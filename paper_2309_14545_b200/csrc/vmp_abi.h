@@ -42,6 +42,8 @@ typedef struct {
  * (chunks >= HBINS-1) and skip absent chunks. */
 #define VMP_HBINS 1024
 #define VMP_QSTRIPES 16           /* item queue striped over 16 counters (t % 16) */
+#define VMP_TRACE_ITEM0 8192      /* debug timeline: per-item records start here */
+#define VMP_TRACE_ITEMS 30000     /* items recorded (4 words each) */
 #define VMP_OFF_CACHE 64          /* round offsets a rake warp keeps in shared memory */
 typedef struct {
   unsigned long long counter[VMP_QSTRIPES * 16]; /* stripe s at [16 s]: one 128 B line each */

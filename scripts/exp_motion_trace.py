@@ -31,7 +31,7 @@ mv()
 torch.cuda.synchronize()
 buf = np.zeros(1 << 16, dtype=np.uint64)
 n = lib().vmp_debug_motion_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.size)
-tr = buf[:n].reshape(-1, 8).astype(np.int64)
+tr = buf[:min(n, 8192)].reshape(-1, 8).astype(np.int64)
 tr = tr[tr[:, 0] > 0]
 t0 = tr[:, 0].min()
 rel = (tr[:, :7] - t0) / 1e3
@@ -45,3 +45,11 @@ hist, edges = np.histogram(w, bins=12)
 print("warp-done histogram:", ", ".join(f"{e:.0f}us:{h}" for e, h in zip(edges, hist)))
 items = tr[:, 7]
 print(f"items per CTA: min {items.min()} median {np.median(items):.0f} max {items.max()}")
+
+# per-item records (start, end, round << 32 | edge, warp << 48 | loop top) of the last launch
+buf = np.zeros(1 << 17, dtype=np.uint64)
+n = lib().vmp_debug_motion_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.size)
+rec = buf[8192:8192 + 4 * 30000].reshape(-1, 4).astype(np.int64)
+rec = rec[(rec[:, 0] >= t0) & (rec[:, 1] > 0)]
+np.savez("gpurun_out/motion_items.npz", rec=rec, t0=t0, cta=tr)
+print("per-item records saved to gpurun_out/motion_items.npz:", len(rec))

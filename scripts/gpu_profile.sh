@@ -14,6 +14,7 @@ cap() {  # cap <name> <kernel regex> <profile_kernels args...>
 }
 cap motion "vmp_motion_p" motion
 cap plan "plan_cluster" motion
+cap finalize "motion_finalize" motion
 cap cfg1 "vmp_validate" cfg1
 cap cfg3 "vmp_validate" cfg3
 cap cfg3_dense "vmp_validate" cfg3 --dense
