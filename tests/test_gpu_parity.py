@@ -351,3 +351,35 @@ def test_motion_plan_paths_agree(cuda, tiles):
                 np.tile(ref_v, tiles).tolist()
             assert n.cpu().numpy().tolist() == np.tile(ref[1].cpu().numpy(), tiles).tolist()
             assert blk.cpu().numpy().tolist() == np.tile(ref[2].cpu().numpy(), tiles).tolist()
+
+
+def test_motion_very_long_edges_and_tiny_batches(cuda):
+    """Edges whose chunk count passes the 1,023-round histogram (n up to ~1e5
+    states: the rounds enumerated past `split`), mixed with short edges, a
+    zero-length edge, and batches of 0 / 1 edges - verdicts, n and W-lane
+    block counts equal the dense oracle's."""
+    mw = workloads.config2()
+    rob = load_robot("arm7")
+    ob = O.Obstacles(mw.env.primitives)
+    rng = np.random.default_rng(7)
+    pick = rng.choice(len(mw.starts), 24, replace=False)
+    s = mw.starts[pick].copy()
+    g = mw.goals[pick].copy()
+    g[3] = s[3]                                          # zero length: n = 1
+    res = 1.0 / 8192.0                                   # n up to ~57,000 states
+    ns = [O.discretization(a, b, res) for a, b in zip(s, g)]
+    assert max(ns) > 32 * 1023, "need edges past the chunk histogram"
+    states = [O.edge_all_states(rob.program, rob.pairs, ob, a, b, res)[1] for a, b in zip(s, g)]
+    for width in (32, 8):
+        ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env, width=width)
+        bits, n, blk = M.validate_motions(ctx, s, g, res, width=width, counts=True)
+        assert n.cpu().numpy().tolist() == ns
+        for i, v in enumerate(states):
+            ok, blocks = O.rake_blocks_from_states(v, width)
+            assert bool(runtime.unpack_bits(bits.cpu().numpy(), len(s))[i]) == ok, i
+            assert int(blk.cpu().numpy()[i]) == blocks, i
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    empty = M.validate_motions(ctx, s[:0], g[:0], res)
+    assert empty.numel() == 0
+    one = M.validate_motions(ctx, s[:1], g[:1], res)
+    assert bool(runtime.unpack_bits(one.cpu().numpy(), 1)[0]) == bool(states[0].all())
