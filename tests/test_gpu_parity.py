@@ -383,3 +383,34 @@ def test_motion_very_long_edges_and_tiny_batches(cuda):
     assert empty.numel() == 0
     one = M.validate_motions(ctx, s[:1], g[:1], res)
     assert bool(runtime.unpack_bits(one.cpu().numpy(), 1)[0]) == bool(states[0].all())
+
+
+@pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5_16"])
+def test_motion_other_robots_vs_oracle(cuda, cfg):
+    """Raked motions of the fetch (8 joints, prismatic torso) and baxter (14
+    joints, two arms) stand-ins in their config-3 / config-4 scenes (mixed
+    spheres, capsules, cuboids; 64-65 obstacles, so two 32-obstacle broadphase
+    chunks per kind run), and arm7 in the 16-primitive config-5 scene: verdicts,
+    n and W-lane block counts (W = 32 and 8, forward and backward) equal the
+    dense oracle's."""
+    wl = workloads.config5(400, 16) if cfg == "cfg5_16" else \
+        {"cfg3": workloads.config3, "cfg4": workloads.config4}[cfg](400)
+    rob = load_robot(wl.robot)
+    q = wl.q.T.copy()                                    # (400, dof)
+    s, g = q[:200], q[200:]
+    res = 1.0 / 16.0
+    ob = O.Obstacles(wl.env.primitives)
+    states = [O.edge_all_states(rob.program, rob.pairs, ob, a, b, res) for a, b in zip(s, g)]
+    ns = [n for n, _ in states]
+    assert 0 < np.mean([v.all() for _, v in states]) < 1
+    for width in (32, 8):
+        for bwd in (False, True):
+            ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env, width=width)
+            bits, n, blk = M.validate_motions(ctx, s, g, res, width=width, backward=bwd,
+                                              counts=True)
+            verdict = runtime.unpack_bits(bits.cpu().numpy(), len(s))
+            assert n.cpu().numpy().tolist() == ns
+            for i, (_, v) in enumerate(states):
+                ok, blocks = O.rake_blocks_from_states(v, width, backward=bwd)
+                assert bool(verdict[i]) == ok, (width, bwd, i)
+                assert int(blk.cpu().numpy()[i]) == blocks, (width, bwd, i)
