@@ -201,10 +201,10 @@ def run_ours(args, rank: int, world: int) -> dict | None:
 
     # ---- end to end through the public API, host buffers: every step copies its
     # edges from pinned host memory and reads its verdict words back; the
-    # 3-slot pipeline (a stream per slot) overlaps step k+1's H2D and rake with step k's drain
+    # 4-slot pipeline (a stream per slot) overlaps step k+1's H2D and rake with step k's drain
     hs = torch.from_numpy(mw.starts).pin_memory()
     hg = torch.from_numpy(mw.goals).pin_memory()
-    depth = 3
+    depth = 4
     pipe = M.MotionPipeline(ctx, E, mw.resolution, width=32, depth=depth)
     for _ in range(args.warmup):
         pipe.result(pipe.submit(hs, hg))
@@ -255,7 +255,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                    "mean_states_per_edge": round(float(n_np.mean()), 2),
                    "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
                    "launch": "CUDA graph (plan -> rake -> finalize, PDL edges) via motion.MotionValidator; "
-                             "e2e through motion.MotionPipeline (3 slots, each step's H2D, "
+                             "e2e through motion.MotionPipeline (4 slots, each step's H2D, "
                              "graph replay and D2H on its slot's own stream: step k+1's copy "
                              "and rake start while step k's rake drains)",
                    "parallelism": f"dp{world} (independent edges per rank)"},

@@ -13,7 +13,10 @@ from paper_2309_14545_b200 import motion as M  # noqa: E402
 torch.cuda.set_device(0)
 mw = workloads.config2()
 rob = load_robot(mw.robot)
-ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+import os  # noqa: E402
+# VMP_EXP_PRUNE=0: contexts without the coarse per-link prune (verdict-neutral)
+ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env,
+                        prune=os.environ.get("VMP_EXP_PRUNE", "1") != "0")
 mv = M.MotionValidator(ctx, len(mw.starts), mw.resolution, width=32)
 mv(mw.starts, mw.goals)
 flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
