@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 20
+CODEGEN_VERSION = 21
 
 
 def f32_literal(value: float) -> str:
@@ -354,8 +354,11 @@ def _state_function(lay: RobotLayout) -> str:
         emit(f"    for (int k0 = sub; k0 < {count}; k0 += 32 * split, p += 32 * split * {f4}) {{")
         emit(f"      const int kn = min(32, ({count} - k0 + split - 1) / split);")
         emit("      unsigned near = 0;")
-        emit("      for (int j = 0; j < kn; ++j) {")
-        emit(f"        const float4 *pp = p + j * split * {f4};")
+        # last obstacle first, the mask shifted up one bit per obstacle: a
+        # pointer step and a shift-or per obstacle, no per-j index arithmetic
+        emit(f"      const float4 *pp = p + (kn - 1) * split * {f4};")
+        emit("#pragma unroll 4")
+        emit(f"      for (int j = kn - 1; j >= 0; --j, pp -= split * {f4}) {{")
         emit(f"        const float4 bnd = pp[{bound}];")
         emit(f"        const float brad = {radius};")
         # one compare per obstacle: the minimum over the groups of the expanded
@@ -364,7 +367,7 @@ def _state_function(lay: RobotLayout) -> str:
             mx, my, mz = _xyz(grp[len(grp) // 2])
             w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
             emit(f"        float wm{gi} = {w};" if gi == 0 else f"        wm0 = fminf(wm0, {w});")
-        emit("        near |= (unsigned)(wm0 <= bnd.w) << j;" if groups else "")
+        emit("        near = (near << 1) | (unsigned)(wm0 <= bnd.w);" if groups else "")
         emit("      }")
         emit("      unsigned todo = __reduce_or_sync(VMP_FULL, near);")
         emit("      while (todo) {")
