@@ -15,10 +15,11 @@ Multi-GPU: one process per GPU (torchrun), every rank validates its own
 4,096-edge batch (weak scaling, no data-path collective - the path shards
 into independent edges); time = max over ranks.
 
-``--impl reference`` times the reference algorithm on the host CPU cores:
-the oracle port (oracle/vecmp_oracle.py, a bit-exact restatement of the
-pure-Python reference) with W = 8 blocks as the reference runs it, one
-process per core, on a bounded sample of the same workload.
+``--impl reference`` times the reference on the host CPU cores: the
+reference package itself (vecmp's own validate_motion_rake, tracing compiler
+and bundled arm7, W = 8 blocks) when it is staged under baseline/_ref/pkg,
+else its bit-exact oracle port (oracle/vecmp_oracle.py); one process per
+core, on a bounded sample of the same workload.
 """
 
 from __future__ import annotations
@@ -362,22 +363,66 @@ def fk_only_summary(ctx_flush, n: int = 1 << 22) -> dict:
 # ------------------------------------------------------- CPU reference arm
 
 _CPU = {}
+# the reference package itself (pure Python / NumPy), staged git-ignored by
+# scripts/run_reference_suite.sh --stage; it travels to the GPU box with the repo
+REF_SRC = ROOT / "baseline" / "_ref" / "pkg" / "src"
+
+
+def _ref_context(mw):
+    """The reference's own ValidationContext(width=8) for config 2: its bundled
+    arm7 URDF / sphere model compiled by its own tracing compiler, the scene
+    converted to its primitive types.  None when the package is not staged."""
+    if not (REF_SRC / "vecmp").is_dir():
+        return None
+    sys.path.insert(0, str(REF_SRC))
+    import vecmp.collision as RC
+    from vecmp.motion import validate_motion_rake
+    from vecmp.planners import build_robot
+    from vecmp.resources import robot_path
+    from vecmp.robot import load_sphere_model, parse_urdf
+    tree = parse_urdf(robot_path("arm7.urdf").read_text())
+    rob = build_robot(tree, load_sphere_model(tree, robot_path("arm7_spheres.yaml").read_text()))
+    prims = []
+    for p in mw.env.primitives:
+        if hasattr(p, "p0"):
+            prims.append(RC.CapsuleObstacle(p0=np.asarray(p.p0, float), p1=np.asarray(p.p1, float),
+                                            radius=float(p.radius)))
+        elif hasattr(p, "half_extents"):
+            prims.append(RC.BoxObstacle(center=np.asarray(p.center, float),
+                                        half_extents=np.asarray(p.half_extents, float),
+                                        rotation=np.asarray(p.rotation, float)))
+        else:
+            prims.append(RC.SphereObstacle(center=np.asarray(p.center, float),
+                                           radius=float(p.radius)))
+    env = RC.Environment(primitives=prims, name=mw.env.name)
+    ctx = RC.ValidationContext(program=rob.program, model=rob.model, pairs=rob.pairs, env=env,
+                               width=8)
+    return ctx, validate_motion_rake
 
 
 def _cpu_init() -> None:
-    """Per-process state of the CPU arm: oracle port, robot program, workload."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import vecmp_oracle as O
+    """Per-process state of the CPU arm: the reference package when staged
+    (kind "reference"), else the oracle port (kind "port"); workload."""
     from paper_2309_14545_b200 import load_robot, workloads
     mw = workloads.config2()
+    ref = _ref_context(mw)
+    if ref is not None:
+        _CPU.update(kind="reference", mw=mw, ctx=ref[0], rake=ref[1])
+        return
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import vecmp_oracle as O
     rob = load_robot(mw.robot)
-    _CPU.update(O=O, mw=mw, rob=rob, ob=O.Obstacles(mw.env.primitives))
+    _CPU.update(kind="port", O=O, mw=mw, rob=rob, ob=O.Obstacles(mw.env.primitives))
 
 
 def _cpu_worker(idx):
     if not _CPU:
         _cpu_init()
-    O, mw, rob, ob = _CPU["O"], _CPU["mw"], _CPU["rob"], _CPU["ob"]
+    mw = _CPU["mw"]
+    if _CPU["kind"] == "reference":
+        ctx, rake = _CPU["ctx"], _CPU["rake"]
+        return [bool(rake(mw.starts[i], mw.goals[i], ctx, mw.resolution)) for i in idx]
+    O, rob, ob = _CPU["O"], _CPU["rob"], _CPU["ob"]
     return [O.rake_check(rob.program, rob.pairs, ob, mw.starts[i], mw.goals[i], mw.resolution, 8)[0]
             for i in idx]
 
@@ -388,16 +433,17 @@ def _sample(n_edges: int, seed: int) -> np.ndarray:
 
 
 def cpu_baseline_motion(mw, rob, processes: int, n_edges: int) -> dict:
-    """Oracle port (bit-exact restatement of the reference) on one host core:
-    the ValidationContext(width=8) rake per edge, as the reference runs it."""
+    """The reference (or, unstaged, its bit-exact oracle port) on one host
+    core: the ValidationContext(width=8) rake per edge, as the reference runs it."""
     _cpu_init()
     idx = _sample(n_edges, 123)
     _cpu_worker(idx[:8])                                  # warm caches
     t0 = time.perf_counter()
     _cpu_worker(idx)
     wall = time.perf_counter() - t0
-    return {"value": round(len(idx) / wall, 2), "unit": "edges/s", "cores": 1, "kind": "port",
-            "sample": f"{len(idx)} seeded-random edges of the 4,096 (W=8 rake, numpy "
+    what = "vecmp validate_motion_rake" if _CPU["kind"] == "reference" else "oracle port"
+    return {"value": round(len(idx) / wall, 2), "unit": "edges/s", "cores": 1, "kind": _CPU["kind"],
+            "sample": f"{len(idx)} seeded-random edges of the 4,096 ({what}, W=8 rake, numpy "
                       f"{np.__version__}, 1 process, {wall:.1f} s wall)"}
 
 
@@ -425,6 +471,9 @@ def run_reference(args, rank: int, world: int) -> dict | None:
         pool.close()
         pool.join()
     value = args.steps * per_step / t_total
+    _cpu_init()                                           # this process: which arm ran
+    kind = _CPU["kind"]
+    what = "vecmp validate_motion_rake" if kind == "reference" else "oracle port of it"
     return {
         "impl": "reference",
         "metric": "validated edges/sec (raked motion validation, BASELINE config 2)",
@@ -434,9 +483,9 @@ def run_reference(args, rank: int, world: int) -> dict | None:
         "data": "synthetic (seeded; arm7 stand-in for Panda)",
         "config": {"workload": mw.name, "robot": "arm7 (Panda stand-in)", "resolution": mw.resolution,
                    "edges_per_step": per_step},
-        "cpu_baseline": {"value": round(value, 2), "unit": "edges/s", "cores": cores, "kind": "port",
-                         "sample": f"{per_step} seeded-random edges per step, W=8 rake, one "
-                                   f"process per core"},
+        "cpu_baseline": {"value": round(value, 2), "unit": "edges/s", "cores": cores, "kind": kind,
+                         "sample": f"{per_step} seeded-random edges per step ({what}), W=8 "
+                                   f"rake, one process per core"},
         "e2e": {"value": round(value, 2), "unit": "edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
