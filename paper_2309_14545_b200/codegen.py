@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 21
+CODEGEN_VERSION = 22
 
 
 def f32_literal(value: float) -> str:
@@ -92,6 +92,7 @@ class RobotLayout:
     coarse: dict       # link -> (radius, xyz) for links with >= 2 fine spheres
     pairs: tuple       # (slot_a, slot_b, thr_f32)
     has_cc: bool       # pairs given -> collision kernels emitted
+    link_pairs: frozenset = frozenset()   # checked (lo, hi) link pairs
 
     @property
     def dynamic(self) -> list:
@@ -128,7 +129,9 @@ def derive_layout(program, pairs=None) -> RobotLayout:
                     pair_list.append((sa, sb, float(thr)))
     return RobotLayout(dof=int(program.dof), n_ops=len(kinds), n_markers=len(program.checks),
                        fine=tuple(fine), coarse=coarse, pairs=tuple(pair_list),
-                       has_cc=pairs is not None)
+                       has_cc=pairs is not None,
+                       link_pairs=frozenset(tuple(sorted(p)) for p in pairs.pairs)
+                       if pairs is not None else frozenset())
 
 
 def _fk_lines(program) -> list[str]:
@@ -234,13 +237,24 @@ def _state_function(lay: RobotLayout) -> str:
     # self-collision pairs (compile-time thresholds), bucketed by group pair;
     # constant spheres are singleton groups with their exact centre and radius.
     # A bucket is skipped when no lane has its two group bounds overlapping.
+    # Buckets of two groups holding spheres of joint-adjacent links (a link
+    # pair with spheres on both links that is not checked) are near in
+    # practically every warp (measured on config 2), so their pairs are tested
+    # without the bucket test.
     group_of: dict[int, tuple] = {}
+    links_of: dict[str, set] = {}
     for gi, grp in enumerate(groups):
         mxyz = _xyz(grp[len(grp) // 2])
         for s in grp:
             group_of[s.slot] = (f"g{gi:03d}", mxyz, f"G{gi}R")
+            links_of.setdefault(f"g{gi:03d}", set()).add(s.link)
     for s in lay.const_spheres:
         group_of[s.slot] = (f"c{s.slot:03d}", _xyz(s), f32_literal(s.radius))
+        links_of.setdefault(f"c{s.slot:03d}", set()).add(s.link)
+
+    def touching(ka, kb):
+        return any(la != lb and (min(la, lb), max(la, lb)) not in lay.link_pairs
+                   for la in links_of[ka] for lb in links_of[kb])
     buckets: dict[tuple, list] = {}
     for sa, sb, thr in lay.pairs:
         ka, kb = group_of[sa][0], group_of[sb][0]
@@ -255,7 +269,7 @@ def _state_function(lay: RobotLayout) -> str:
             bx, by, bz = _xyz(fine[sb])
             tests.append(f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, "
                          f"{f32_literal(thr)}); ")
-        if ka == kb or (ka[0] == "c" and kb[0] == "c"):
+        if ka == kb or (ka[0] == "c" and kb[0] == "c") or touching(ka, kb):
             for t in tests:
                 emit("  " + t)
             continue
