@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 22
+CODEGEN_VERSION = 23
 
 
 def f32_literal(value: float) -> str:
@@ -348,12 +348,15 @@ def _state_function(lay: RobotLayout) -> str:
         # batch validation: one pass, a warp vote per obstacle on the group bounds
         emit(f"    for (int k = sub; k < {count}; k += split, p += split * {f4}) {{")
         emit(f"      const float4 {loads};")
-        emit("      bool nr = false;")
+        # near iff the minimum over the groups of the expanded bound distance
+        # is <= the threshold: one compare per obstacle
+        emit(f"      const float4 bnd = p[{bound}];")
+        emit(f"      const float brad = {radius.replace('pp[', 'p[')};")
         for gi, grp in enumerate(groups):
             mx, my, mz = _xyz(grp[len(grp) // 2])
-            emit(f"      nr |= !vmp_clear_sphere({mx}, {my}, {mz}, G{gi}S, G{gi}M, p[{bound}], "
-                 f"{radius.replace('pp[', 'p[')});")
-        emit("      if (__any_sync(VMP_FULL, nr)) {")
+            w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
+            emit(f"      float wm{gi} = {w};" if gi == 0 else f"      wm0 = fminf(wm0, {w});")
+        emit("      if (__any_sync(VMP_FULL, wm0 <= bnd.w)) {")
         group_tests(test_fn, coarse_fn, "        ")
         emit("      }")
         emit("      if ((k & VMP_STOP_MASK) == VMP_STOP_MASK && VMP_STOP_NOW) return ok;")
