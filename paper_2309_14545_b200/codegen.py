@@ -58,7 +58,10 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 23
+CODEGEN_VERSION = 24
+# per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
+# this before codegen runs); off in production - they cost ~2 % of the step
+TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
 
 
 def f32_literal(value: float) -> str:
@@ -442,6 +445,15 @@ def _const_check(lay: RobotLayout) -> str:
     return "\n".join(lines)
 
 
+_TRACE_BLOCK = """    if (trace && lane == 0 && t < VMP_TRACE_ITEMS) {   // per item: start, end, round | edge, warp | top
+      unsigned long long *rec = a.trace + VMP_TRACE_ITEM0 + 4 * t;
+      rec[0] = t_start;
+      rec[1] = vmp_gtime();
+      rec[2] = ((unsigned long long)ci << 32) | (unsigned long long)ei;
+      rec[3] = ((unsigned long long)wid << 48) | (t_top & 0xffffffffffffull);
+    }"""
+
+
 def _kernels(lay: RobotLayout, program) -> str:
     dofp = max(1, lay.dof)
     ld_q = "\n".join(f"    q[{j}] = __ldg(a.q + {j} * a.ld + ii);" for j in range(lay.dof))
@@ -644,7 +656,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   unsigned long long grab = 0;
   bool have = false;
   for (;;) {{
-    const unsigned long long t_top = trace ? vmp_gtime() : 0;
+{"    const unsigned long long t_top = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
     if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
     const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
     have = false;
@@ -706,7 +718,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
     // the native width (W = 32: chunk c is iteration c + 1) skips the divisions
     const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
     const int fe = __ldcg(a.fail_enc + ei);  // 0, or INT_MAX - first failing iteration
-    const unsigned long long t_start = trace ? vmp_gtime() : 0;
+{"    const unsigned long long t_start = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
     if (fe == 0 || 0x7fffffff - fe > (int)first_iter) {{   // else: cannot lower the count
       float s[{dofp}], g[{dofp}];
 #pragma unroll
@@ -731,13 +743,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
         atomicMax(a.fail_enc + ei, 0x7fffffff - (int)it);
       }}
     }}
-    if (trace && lane == 0 && t < VMP_TRACE_ITEMS) {{   // per item: start, end, round | edge, warp | top
-      unsigned long long *rec = a.trace + VMP_TRACE_ITEM0 + 4 * t;
-      rec[0] = t_start;
-      rec[1] = vmp_gtime();
-      rec[2] = ((unsigned long long)ci << 32) | (unsigned long long)ei;
-      rec[3] = ((unsigned long long)wid << 48) | (t_top & 0xffffffffffffull);
-    }}
+{_TRACE_BLOCK if TRACE_ITEMS else ""}
 
   }}
   if (trace && threadIdx.x == 0) trace[6] = vmp_gtime();

@@ -1,11 +1,16 @@
 """Timeline of one config-2 rake launch (run with VMP_MOTION_TRACE=1): when CTAs
-start, when the plan is ready, when each warp finds the queue empty, CTA exit.
+start, when the plan is ready, when each warp finds the queue empty, CTA exit,
+and per-item records (a debug build of the rake: VMP_MOTION_TRACE_ITEMS=1 is
+set here before codegen runs, so the module is compiled by NVRTC on first use).
 
     VMP_MOTION_TRACE=1 python scripts/exp_motion_trace.py
 """
 import ctypes
+import os
 import sys
 from pathlib import Path
+
+os.environ["VMP_MOTION_TRACE_ITEMS"] = "1"
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np  # noqa: E402
