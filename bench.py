@@ -496,7 +496,7 @@ def run_reference(args, rank: int, world: int) -> dict | None:
 def main() -> None:
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
     p.add_argument("--no-aux", action="store_true", help="skip the FK+CC batch summary")
