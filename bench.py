@@ -262,10 +262,11 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                    "parallelism": f"dp{world} (independent edges per rank)"},
         "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                     "traffic": _traffic("vmp_motion_p1_s2_g1_o"),
-                     # the register-capped rake variant, loaded when it compiles
-                     # without local memory (arm7: 96 registers, 5 CTAs / SM)
-                     "kernel": "vmp_motion_p1_s2_g1_o",
+                     "traffic": _traffic("vmp_motion_p1_s2_g1_o_ns"),
+                     # the register-capped rake variant (loaded when it compiles
+                     # without local memory; arm7: 96 registers, 5 CTAs / SM),
+                     # built without sphere-obstacle code (config 2 has none)
+                     "kernel": "vmp_motion_p1_s2_g1_o_ns",
                      "algorithmic_flop_per_state": f_state,
                      "states_counted_per_launch": int(states.sum()),
                      "note": "states fully evaluated by the rake (valid edges: all n; invalid: "

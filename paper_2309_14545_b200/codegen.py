@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 24
+CODEGEN_VERSION = 25
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
 # this before codegen runs); off in production - they cost ~2 % of the step
 TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
@@ -185,7 +185,7 @@ def _state_function(lay: RobotLayout) -> str:
     dyn = lay.dynamic
     out = []
     emit = out.append
-    emit("template <int STOP, bool PRUNE, bool TWO = (STOP == 2)>")
+    emit("template <int STOP, bool PRUNE, bool TWO = (STOP == 2), bool NO_SPH = false>")
     emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
     emit("                                          int ns, int nc, int nb, bool ok,")
     emit("                                          int sub = 0, int split = 1,")
@@ -405,8 +405,12 @@ def _state_function(lay: RobotLayout) -> str:
         # the environment copy (cp.async.bulk) was in flight during FK and self pairs
         emit("  if (bar) vmp_mbar_wait(bar, 0);")
         emit("  const float4 *p = env;")
+        # NO_SPH: the rake variant for scenes without sphere obstacles carries no
+        # sphere code (a smaller hot loop for the instruction cache)
+        emit("  if constexpr (!NO_SPH) {")
         kind_loop("ns", "VMP_SPH_F4", "env", "r0 = p[0], r1 = p[1]", "0", "pp[1].x",
                   sph_test, sph_coarse)
+        emit("  }")
         kind_loop("nc", "VMP_CAP_F4", "(env + VMP_SPH_F4 * ns)", "r0 = p[0], r1 = p[1], r2 = p[2]",
                   "3", "pp[2].w", cap_test, cap_coarse)
         kind_loop("nb", "VMP_BOX_F4", "(env + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc)",
@@ -606,7 +610,7 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   if (STAGED && !cdone) vmp_mbar_wait(&vmp_bar, 0);   // no tile: still retire the copy
 }}
 
-template <int PRUNE, int STOP, bool STAGED>
+template <int PRUNE, int STOP, bool STAGED, bool NO_SPH = false>
 __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // Work items are (chunk c, edge e) pairs enumerated round by round (c-major,
   // dense).  Chunk c is rake positions [32c, 32c + 32) of the W-lane rake
@@ -736,7 +740,8 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       float q[{dofp}];
 #pragma unroll
       for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
-      const bool ok = vmp_state<STOP, PRUNE != 0>(q, env, a.env.ns, a.env.nc, a.env.nb, inr && cclear);
+      const bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc,
+                                                                  a.env.nb, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
       if (bad && lane == 0) {{
         const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
@@ -775,6 +780,9 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
                         f'vmp_motion_p{prune}_s2_g1_o(VmpMotionArgs a) '
                         f'{{ vmp_motion_body<{prune}, 2, true>(a); }}\n')
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
+                        f'vmp_motion_p{prune}_s2_g1_o_ns(VmpMotionArgs a) '
+                        f'{{ vmp_motion_body<{prune}, 2, true, true>(a); }}\n')
     return src
 
 
