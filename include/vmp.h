@@ -40,6 +40,8 @@ extern "C" {
 #define VMP_TWO_PASS 64u     /* two-pass broadphase (bound mask per 32 obstacles)     */
 /* vmp_validate_motions flags (reference motion.py:38-90) */
 #define VMP_BACKWARD 16u     /* comb each stratum top-down (backward=True)            */
+#define VMP_OVERLAPPED 512u  /* batches overlap on several streams (a pipeline):
+                                keep prefetching work items until the queue's end  */
 
 typedef struct vmp_robot vmp_robot; /* compiled module for one KinematicProgram (+pairs) */
 typedef struct vmp_env vmp_env;     /* device-resident packed obstacles                   */

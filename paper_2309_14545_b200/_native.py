@@ -30,6 +30,7 @@ VMP_NO_SPLIT = 8
 VMP_FORCE_SPLIT = 32
 VMP_TWO_PASS = 64
 VMP_BACKWARD = 16
+VMP_OVERLAPPED = 512
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 25
+CODEGEN_VERSION = 26
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
 # this before codegen runs); off in production - they cost ~2 % of the step
 TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
@@ -654,9 +654,12 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   int stripe = wid % VMP_QSTRIPES, dry = 0;
   // the next item's atomic is issued before the current chunk is evaluated
-  // (hides the L2 atomic round trip) unless the queue is nearly drained, where
-  // holding a reserved item would lengthen the tail
-  const long long guard = (long long)gridDim.x * (blockDim.x >> 5);
+  // (hides the L2 atomic round trip) unless the queue is within guard_waves
+  // items per warp of its end, where holding a reserved item lengthens the
+  // tail of an isolated batch (1 / 2 / 4 / 8 items per warp: 47.1 / 46.1 /
+  // 45.05 / 45.1 us); overlapped batches fill each other's tails (1: 38.1 us
+  // per pipelined step, 4: 39.2)
+  const long long guard = (long long)a.guard_waves * gridDim.x * (blockDim.x >> 5);
   unsigned long long grab = 0;
   bool have = false;
   for (;;) {{

@@ -73,7 +73,9 @@ typedef struct {
   int width;            /* rake lane width W whose block counts are reproduced */
   int backward;         /* comb strata top-down */
   int stage;
-  int pad_;
+  int guard_waves;      /* stop prefetching queue items this many items per warp
+                           before the end (4 for an isolated batch; 1 when batches
+                           overlap, whose tails the next batch fills) */
 } VmpMotionArgs;
 
 typedef struct {

@@ -100,11 +100,13 @@ class MotionValidator:
     """
 
     def __init__(self, ctx: ValidationContext, n_edges: int, resolution: float, *,
-                 width: int = 32, backward: bool = False, graph: bool = True):
+                 width: int = 32, backward: bool = False, graph: bool = True,
+                 overlapped: bool = False):
         _check_resolution(resolution)
         torch = runtime.require_cuda()
         self.ctx, self.n_edges, self.resolution = ctx, int(n_edges), float(resolution)
         self.width, self.backward = int(width), bool(backward)
+        self.overlapped = bool(overlapped)     # runs next to other batches (pipeline)
         dof = ctx.program.dof
         dev = torch.cuda.current_device()
         self.starts = torch.zeros((self.n_edges, dof), dtype=torch.float32, device=dev)
@@ -126,7 +128,8 @@ class MotionValidator:
         runtime.validate_motions_device(self._mod, self._denv, self.starts, self.goals,
                                         self.resolution, width=self.width,
                                         backward=self.backward, prune=getattr(self.ctx, "prune", True),
-                                        bits=self.bits, workspace=self.workspace)
+                                        bits=self.bits, workspace=self.workspace,
+                                        overlapped=self.overlapped)
 
     def __call__(self, starts=None, goals=None):
         if starts is not None:
@@ -170,7 +173,8 @@ class MotionPipeline:
                  width: int = 32, depth: int = 3):
         torch = runtime.require_cuda()
         self.torch = torch
-        self.slots = [MotionValidator(ctx, n_edges, resolution, width=width) for _ in range(depth)]
+        self.slots = [MotionValidator(ctx, n_edges, resolution, width=width, overlapped=True)
+                      for _ in range(depth)]
         self.streams = [torch.cuda.Stream() for _ in self.slots]
         origin = torch.cuda.current_stream()
         self.host = [torch.empty(s.bits.shape, dtype=torch.int32).pin_memory() for s in self.slots]
