@@ -79,6 +79,15 @@ void vmp_robot_destroy(vmp_robot *robot);
  */
 int vmp_env_create(const double *spheres, int32_t n_spheres, const double *capsules,
                    int32_t n_capsules, const double *boxes, int32_t n_boxes, vmp_env **out);
+/* Same, with the records expressed in a frame centred at `origin` (3 doubles,
+ * rounded to float32; NULL = world origin).  Kernels subtract the origin from
+ * every sphere centre before the environment tests, so with an origin near the
+ * robot the expanded test forms never cancel |c|^2-sized terms (a robot 30 m
+ * from the world origin keeps the same accuracy as one at the origin).
+ * Verdict semantics are unchanged (reference collision.py:206-254). */
+int vmp_env_create_at(const double *spheres, int32_t n_spheres, const double *capsules,
+                      int32_t n_capsules, const double *boxes, int32_t n_boxes,
+                      const double *origin, vmp_env **out);
 void vmp_env_destroy(vmp_env *env);
 /* Bytes of the packed device records (shared-memory staging size). */
 int64_t vmp_env_bytes(const vmp_env *env);
@@ -110,7 +119,10 @@ int vmp_validate(const vmp_robot *robot, const vmp_env *env, const float *q, int
  *   blocks     : optional, block evaluations the W-wide rake performs
  *   workspace  : >= vmp_motion_workspace_bytes(n_edges) bytes of device
  *                scratch (work queue + per-edge plan); 16-byte aligned and
- *                ZERO-FILLED before its first use (calls leave it zeroed)
+ *                ZERO-FILLED before its first use.  Its layout depends only
+ *                on workspace_bytes, so one workspace serves batches of any
+ *                size it holds; each call resets the queue counters itself
+ *                and re-zeroes its edges' failure records when it finishes
  * Launches plan -> fused FK+CC rake -> finalize on `stream`. */
 int vmp_validate_motions(const vmp_robot *robot, const vmp_env *env, const float *starts,
                          const float *goals, int64_t n_edges, int64_t sld, double resolution,

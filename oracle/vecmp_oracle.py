@@ -349,6 +349,20 @@ def _box_dist(p, centre, half, rot):
     return np.linalg.norm(local - clamped, axis=0)
 
 
+def primitive_gap_f64(p, c: np.ndarray, radius: float) -> np.ndarray:
+    """float64 signed gap between spheres of ``radius`` at points c (3, n) and
+    one primitive (closest-point forms of pkg/tests/test_collision.py:24-39)."""
+    kind = _kind(p)
+    if kind == "sphere":
+        d = np.linalg.norm(c - np.asarray(p.center, float)[:, None], axis=0)
+        return d - (float(p.radius) + radius)
+    if kind == "capsule":
+        return _seg_dist(c, np.asarray(p.p0, float), np.asarray(p.p1, float)) \
+            - (float(p.radius) + radius)
+    return _box_dist(c, np.asarray(p.center, float), np.asarray(p.half_extents, float),
+                     np.asarray(p.rotation, float)) - radius
+
+
 def clearance_f64(program, pairs, primitives, q: np.ndarray) -> np.ndarray:
     """Minimum signed clearance (m) per configuration, float64.
 
@@ -367,17 +381,7 @@ def clearance_f64(program, pairs, primitives, q: np.ndarray) -> np.ndarray:
         c = rows[list(m.xyz)]
         cen.setdefault(m.link, []).append((c, m.radius))
         for p in primitives:
-            kind = _kind(p)
-            if kind == "sphere":
-                d = np.linalg.norm(c - np.asarray(p.center, float)[:, None], axis=0)
-                gap = d - (float(p.radius) + m.radius)
-            elif kind == "capsule":
-                gap = _seg_dist(c, np.asarray(p.p0, float), np.asarray(p.p1, float)) \
-                    - (float(p.radius) + m.radius)
-            else:
-                gap = _box_dist(c, np.asarray(p.center, float), np.asarray(p.half_extents, float),
-                                np.asarray(p.rotation, float)) - m.radius
-            np.minimum(best, gap, out=best)
+            np.minimum(best, primitive_gap_f64(p, c, m.radius), out=best)
     for a, b in pairs.pairs:
         for ca, ra in cen.get(a, ()):
             for cb, rb in cen.get(b, ()):

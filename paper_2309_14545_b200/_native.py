@@ -41,7 +41,8 @@ NVCC_FLAGS = [
 #: every symbol include/vmp.h declares (checked by the CPU tests)
 EXPORTS = (
     "vmp_version", "vmp_last_error", "vmp_compile", "vmp_robot_load", "vmp_robot_destroy",
-    "vmp_env_create", "vmp_env_destroy", "vmp_env_bytes", "vmp_fk_rows", "vmp_fk_spheres",
+    "vmp_env_create", "vmp_env_create_at", "vmp_env_destroy", "vmp_env_bytes", "vmp_fk_rows",
+    "vmp_fk_spheres",
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
     "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace",
@@ -100,6 +101,8 @@ def lib() -> ctypes.CDLL:
         "vmp_robot_load": ([cp, ctypes.POINTER(RobotDesc), ctypes.POINTER(vp)], ctypes.c_int),
         "vmp_robot_destroy": ([vp], None),
         "vmp_env_create": ([vp, c_i32, vp, c_i32, vp, c_i32, ctypes.POINTER(vp)], ctypes.c_int),
+        "vmp_env_create_at": ([vp, c_i32, vp, c_i32, vp, c_i32, vp, ctypes.POINTER(vp)],
+                              ctypes.c_int),
         "vmp_env_destroy": ([vp], None),
         "vmp_env_bytes": ([vp], c_i64),
         "vmp_fk_rows": ([vp, vp, c_i64, c_i64, vp, c_i64, vp], ctypes.c_int),

@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 26
+CODEGEN_VERSION = 27
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
 # this before codegen runs); off in production - they cost ~2 % of the step
 TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
@@ -181,20 +181,36 @@ def _xyz(s: FineSphere) -> tuple[str, str, str]:
     return tuple(f"v{v}" for v in s.xyz)
 
 
+def _exyz(s: FineSphere) -> tuple[str, str, str]:
+    """Centre of a dynamic sphere in the environment's frame (minus its origin)."""
+    return tuple(f"E{s.slot}{axis}" for axis in "xyz")
+
+
 def _state_function(lay: RobotLayout) -> str:
     dyn = lay.dynamic
     out = []
     emit = out.append
     emit("template <int STOP, bool PRUNE, bool TWO = (STOP == 2), bool NO_SPH = false>")
     emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
-    emit("                                          int ns, int nc, int nb, bool ok,")
+    emit("                                          int ns, int nc, int nb, float3 org, bool ok,")
     emit("                                          int sub = 0, int split = 1,")
     emit("                                          unsigned long long *bar = nullptr) {")
     emit("  // split > 1: this thread handles obstacles k = sub (mod split) and self")
     emit("  // pairs i = sub (mod split) of its configuration (small-batch kernels)")
-    emit("  (void)env; (void)ns; (void)nc; (void)nb;")
+    emit("  (void)env; (void)ns; (void)nc; (void)nb; (void)org;")
     for line in _FK_BODY_PLACEHOLDER:
         emit(line)
+    # environment tests run in the environment's frame: centres minus the
+    # env origin (records are packed relative to it), so the expanded test
+    # forms never cancel |c|^2-sized terms for a robot far from the world
+    # origin; self pairs and group radii use differences and stay in world
+    # coordinates
+    for s in lay.dynamic:
+        for axis, v in zip("xyz", s.xyz):
+            emit(f"  const float E{s.slot}{axis} = v{v} - org.{axis};")
+    for link, (_, xyz) in lay.coarse.items():
+        for axis, v in zip("xyz", xyz):
+            emit(f"  const float K{link}{axis} = v{v} - org.{axis};")
     emit("#define VMP_STOP_NOW ((STOP == 1 && !__any_sync(VMP_FULL, ok)) || "
          "(STOP == 2 && __any_sync(VMP_FULL, !ok && vmp_inr)))")
     emit("  const bool vmp_inr = ok;")
@@ -216,7 +232,7 @@ def _state_function(lay: RobotLayout) -> str:
     emit("  }")
     # per-sphere constants
     for s in dyn:
-        x, y, z = _xyz(s)
+        x, y, z = _exyz(s)
         rs2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
         emit(f"  const float S{s.slot} = vmp_sphere_S({x}, {y}, {z}, {f32_literal(rs2)});")
     # broadphase groups: consecutive dynamic spheres, bounded per lane by a sphere
@@ -235,7 +251,8 @@ def _state_function(lay: RobotLayout) -> str:
             emit(f"  G{gi}R = fmaxf(G{gi}R, vmp_dist({x}, {y}, {z}, {mx}, {my}, {mz}) + "
                  f"{f32_literal(s.radius)});")
         emit(f"  G{gi}R = fmaf(G{gi}R, 1.000002f, 1e-6f);")
-        emit(f"  const float G{gi}S = vmp_sphere_S({mx}, {my}, {mz}, G{gi}R * G{gi}R);")
+        ex, ey, ez = _exyz(mid)
+        emit(f"  const float G{gi}S = vmp_sphere_S({ex}, {ey}, {ez}, G{gi}R * G{gi}R);")
         emit(f"  const float G{gi}M = -2.0f * G{gi}R;")
     # self-collision pairs (compile-time thresholds), bucketed by group pair;
     # constant spheres are singleton groups with their exact centre and radius.
@@ -302,11 +319,11 @@ def _state_function(lay: RobotLayout) -> str:
                     emit(ind + "ok &= " + t + ";")
 
     def coarse_xyz(link):
-        r, xyz = lay.coarse[link]
-        return r, tuple(f"v{v}" for v in xyz)
+        r, _ = lay.coarse[link]
+        return r, tuple(f"K{link}{axis}" for axis in "xyz")
 
     def sph_test(s):
-        x, y, z = _xyz(s)
+        x, y, z = _exyz(s)
         return f"vmp_clear_sphere({x}, {y}, {z}, S{s.slot}, {f32_literal(-2.0 * np.float32(s.radius))}, r0, r1.x)"
 
     def sph_coarse(link):
@@ -316,7 +333,7 @@ def _state_function(lay: RobotLayout) -> str:
                 f"{f32_literal(-2.0 * np.float32(r))}, r0, r1.x)")
 
     def cap_test(s):
-        x, y, z = _xyz(s)
+        x, y, z = _exyz(s)
         return f"vmp_clear_capsule({x}, {y}, {z}, S{s.slot}, {f32_literal(-2.0 * np.float32(s.radius))}, r0, r1, r2)"
 
     def cap_coarse(link):
@@ -329,7 +346,7 @@ def _state_function(lay: RobotLayout) -> str:
         return "vmp_clear_box_small" if radius < 1.0 else "vmp_clear_box_any"
 
     def box_test(s):
-        x, y, z = _xyz(s)
+        x, y, z = _exyz(s)
         rs2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
         return f"{box_fn(s.radius)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
 
@@ -356,7 +373,7 @@ def _state_function(lay: RobotLayout) -> str:
         emit(f"      const float4 bnd = p[{bound}];")
         emit(f"      const float brad = {radius.replace('pp[', 'p[')};")
         for gi, grp in enumerate(groups):
-            mx, my, mz = _xyz(grp[len(grp) // 2])
+            mx, my, mz = _exyz(grp[len(grp) // 2])
             w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
             emit(f"      float wm{gi} = {w};" if gi == 0 else f"      wm0 = fminf(wm0, {w});")
         emit("      if (__any_sync(VMP_FULL, wm0 <= bnd.w)) {")
@@ -384,7 +401,7 @@ def _state_function(lay: RobotLayout) -> str:
         # one compare per obstacle: the minimum over the groups of the expanded
         # bound distance (near iff some group's is <= the threshold)
         for gi, grp in enumerate(groups):
-            mx, my, mz = _xyz(grp[len(grp) // 2])
+            mx, my, mz = _exyz(grp[len(grp) // 2])
             w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
             emit(f"        float wm{gi} = {w};" if gi == 0 else f"        wm0 = fminf(wm0, {w});")
         emit("        near = (near << 1) | (unsigned)(wm0 <= bnd.w);" if groups else "")
@@ -428,8 +445,9 @@ _FK_BODY_PLACEHOLDER = ["  VMP_FK_BODY"]
 def _const_check(lay: RobotLayout) -> str:
     """Per-CTA test of configuration-independent spheres against the env."""
     consts = lay.const_spheres
-    lines = ["__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb) {",
-             "  (void)env; (void)ns; (void)nc; (void)nb;",
+    lines = ["__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb,",
+             "                                                float3 org) {",
+             "  (void)env; (void)ns; (void)nc; (void)nb; (void)org;",
              "  bool ok = true;"]
     if consts:
         # (const sphere, obstacle) pairs spread over the CTA's threads
@@ -440,7 +458,8 @@ def _const_check(lay: RobotLayout) -> str:
         for k, s in enumerate(consts):
             # centre coordinates of a const sphere are CONST ops: exact float32 literals
             lines.append(f"    case {k}: ok &= vmp_sphere_clear_obstacle(env, ns, nc, nb, k, "
-                         f"VMP_C{s.slot}X, VMP_C{s.slot}Y, VMP_C{s.slot}Z, {f32_literal(s.radius)}); break;")
+                         f"VMP_C{s.slot}X - org.x, VMP_C{s.slot}Y - org.y, VMP_C{s.slot}Z - org.z, "
+                         f"{f32_literal(s.radius)}); break;")
         lines.append("    default: break;")
         lines.append("    }")
         lines.append("  }")
@@ -570,6 +589,7 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   // the environment copy overlaps the joint loads, FK and self pairs of the
   // first tile; vmp_state waits for it before the first obstacle
   const float4 *env = STAGED ? vmp_smem : a.env.rec;
+  const float3 org = make_float3(a.env.ox, a.env.oy, a.env.oz);
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
     __syncthreads();
@@ -584,11 +604,11 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
     const long long ii = inr ? i : a.n - 1;
     float q[{dofp}];
 {ld_q}
-    bool ok = vmp_state<STOP, PRUNE != 0, TWO>(q, env, a.env.ns, a.env.nc, a.env.nb, inr, sub,
+    bool ok = vmp_state<STOP, PRUNE != 0, TWO>(q, env, a.env.ns, a.env.nc, a.env.nb, org, inr, sub,
                                                SPLIT, STAGED ? &vmp_bar : nullptr);
     if (!cdone) {{                            // CTA-uniform: once, after the first tile
       if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
-      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, org));
       cdone = true;
     }}
     ok = ok && cclear;
@@ -632,13 +652,14 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // retire and wait (griddepcontrol.wait) for this whole grid
   asm volatile("griddepcontrol.launch_dependents;");
   const float4 *env = a.env.rec;
+  const float3 org = make_float3(a.env.ox, a.env.oy, a.env.oz);
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
     __syncthreads();
     vmp_mbar_wait(&vmp_bar, 0);
     env = vmp_smem;
   }}
-  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, org));
   if (trace && threadIdx.x == 0) trace[1] = vmp_gtime();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long E = a.n_edges;
@@ -744,7 +765,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
 #pragma unroll
       for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
       const bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc,
-                                                                  a.env.nb, inr && cclear);
+                                                                  a.env.nb, org, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
       if (bad && lane == 0) {{
         const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;

@@ -15,6 +15,9 @@ typedef struct {
   const float4 *rec;   /* device pointer, 16-byte aligned */
   int ns, nc, nb;      /* sphere / capsule / cuboid counts */
   int n_f4;            /* total float4 records = 2 ns + 4 nc + 5 nb */
+  float ox, oy, oz;    /* origin of the environment frame: records hold obstacle
+                          geometry minus it, kernels subtract it from sphere centres */
+  int pad_;
 } VmpEnvView;
 
 typedef struct {
@@ -27,15 +30,18 @@ typedef struct {
   int pad_;
 } VmpValidateArgs;
 
-/* Motion workspace (zero-filled once by the caller; every call leaves it zero):
+/* Motion workspace (zero-filled once by the caller; the per-edge arrays are
+ * laid out by the capacity the workspace size implies, E_cap; every call
+ * resets the queue counters before the rake starts and re-zeroes fail_enc of
+ * its edges in finalize):
  *   VmpMotionHeader
  *   unsigned hist[VMP_HBINS], fill[VMP_HBINS]   chunk-count histogram / scatter cursors
  *   long long off[VMP_HBINS]                    first work item of chunk round c
- *   int fail_enc[E]                             per edge: INT_MAX - first failing
+ *   int fail_enc[E_cap]                         per edge: INT_MAX - first failing
  *                                               iteration, 0 while none
- *   int n[E], chunks[E]                         per edge: discretisation count (rake
+ *   int n[E_cap], chunks[E_cap]                 per edge: discretisation count (rake
  *                                               round 0); chunks (multi-kernel plan)
- *   int4 order[E]                               (edge, n, chunks, 0) by chunk count desc
+ *   int4 order[E_cap]                           (edge, n, chunks, 0) by chunk count desc
  * Work item t < E is round 0 of edge t (input order, no plan needed); item
  * E <= t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c, where
  * off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest edges

@@ -38,7 +38,8 @@ def _pair(start: Config, goal: Config) -> tuple[np.ndarray, np.ndarray]:
 def _bind(ctx):
     """(robot module, device env) for any context exposing program/pairs/env
     (ours, or a reference ValidationContext built before patch_vecmp)."""
-    return (runtime.robot_module(ctx.program, ctx.pairs), runtime.device_env(ctx.env))
+    mod = runtime.robot_module(ctx.program, ctx.pairs)
+    return mod, runtime.device_env(ctx.env, mod.home)
 
 
 def _check_resolution(resolution: float) -> None:
@@ -205,6 +206,12 @@ class MotionPipeline:
             stream.wait_stream(st)
 
     def result(self, ticket: int):
+        """Verdict words of batch ``ticket``; only the last ``depth`` batches are held
+        (a slot's buffer is overwritten by the submit ``depth`` tickets later)."""
+        if not (self.count - len(self.slots) <= ticket < self.count):
+            raise ValueError(f"ticket {ticket} is not held: the pipeline holds the last "
+                             f"{len(self.slots)} batches ({max(self.count - len(self.slots), 0)}"
+                             f"..{self.count - 1})")
         k = ticket % len(self.slots)
         self.done[k].synchronize()
         return self.host[k].numpy()

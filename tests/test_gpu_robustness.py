@@ -1,0 +1,231 @@
+"""GPU parity beyond the benchmark shapes (VERDICT r1 "what's weak"):
+
+* the kernel variants the config-5 sweep actually runs at large N (single
+  thread per configuration, product ``s1`` and dense ``s0``) at P = 128 and
+  1,024 primitives, N = 65,536 (whole batch vs the oracle), 2^20 and 2^24
+  (8,192-configuration oracle samples);
+* a motion batch in the 1,024-primitive scene, and scenes too large to stage
+  in shared memory (unstaged global reads);
+* translated scenes: robot base and obstacles moved 5, 10 and 30 m from the
+  world origin (the expanded narrowphase forms run in an environment frame
+  centred near the robot, vmp_env_create_at);
+* one motion workspace reused across batch sizes, and a workspace whose queue
+  counters were left dirty.
+
+Bars as in test_gpu_parity.py: verdicts bit-identical to the oracle outside
+the +-1e-4 m clearance band, in-band mismatches counted; motion verdicts
+identical.
+"""
+
+import numpy as np
+import pytest
+
+import vecmp_oracle as O
+from paper_2309_14545_b200 import ValidationContext, load_robot, runtime, workloads
+from paper_2309_14545_b200 import motion as M
+from program_tools import translate_env, translate_program
+
+pytestmark = pytest.mark.gpu
+
+BAND = 1e-4
+
+
+def _parity(program, pairs, prims, q, got, *, max_band=None):
+    ref = O.validate_configs(program, pairs, prims, q)
+    clear = O.clearance_f64(program, pairs, prims, q)
+    outside = np.abs(clear) > BAND
+    bad = np.flatnonzero(outside & (got != ref))
+    assert bad.size == 0, f"{bad.size} verdicts differ outside the band, e.g. {bad[:5]}"
+    band = int(np.sum(~outside & (got != ref)))
+    if max_band is not None:
+        assert band <= max_band, f"{band} in-band mismatches"
+    return band
+
+
+def _edge_oracle(program, pairs, prims, starts, goals, resolution):
+    ob = O.Obstacles(prims)
+    return np.array([bool(O.edge_all_states(program, pairs, ob, s, g, resolution)[1].all())
+                     for s, g in zip(starts, goals)])
+
+
+# ------------------------------------------------- large-N kernel variants
+
+@pytest.mark.parametrize("p", [128, 1024])
+@pytest.mark.parametrize("dense", [False, True])
+def test_single_thread_kernels_vs_oracle_65536(cuda, p, dense):
+    """s1 (product: broadphase + early exit) and s0 (dense) single-thread
+    kernels - the ones the sweep runs above 16,384 configurations."""
+    torch = cuda
+    wl = workloads.config5(65536, p)
+    rob = load_robot(wl.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    qd = torch.from_numpy(wl.q).cuda()
+    words = runtime.validate_device(ctx.module, ctx.device_env, qd, qd.shape[1], qd.shape[1],
+                                    early_exit=not dense, split=False)
+    got = runtime.unpack_bits(words.cpu().numpy(), qd.shape[1])
+    _parity(rob.program, rob.pairs, wl.env.primitives, wl.q, got, max_band=8)
+
+
+@pytest.mark.parametrize("p", [16, 128, 1024])
+@pytest.mark.parametrize("log_n", [20, 24])
+def test_sweep_sizes_sampled_vs_oracle(cuda, p, log_n):
+    """The sweep's large points: product and dense agree on every verdict,
+    and an 8,192-configuration sample matches the oracle."""
+    torch = cuda
+    n = 1 << log_n
+    rob = load_robot("arm7")
+    env = workloads.config5_scene(p)
+    q = workloads.uniform_configs(rob.limits, n, 50)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env)
+    qd = torch.from_numpy(q).cuda()
+    del q
+    prod = ctx.validate_batch(qd).cpu().numpy()
+    if p * n <= (1 << 31):     # dense at 2^24 x 1,024 would take ~100 s
+        dense = ctx.validate_batch(qd, early_exit=False).cpu().numpy()
+        assert np.array_equal(prod, dense)
+    idx = np.sort(np.random.default_rng(log_n * 7 + p).choice(n, 8192, replace=False))
+    sample = qd[:, torch.from_numpy(idx).cuda()].cpu().numpy()
+    got = runtime.unpack_bits(prod, n)[idx]
+    _parity(rob.program, rob.pairs, env.primitives, sample, got, max_band=4)
+
+
+def test_motion_in_1024_primitive_scene(cuda):
+    rob = load_robot("arm7")
+    env = workloads.config5_scene(1024)
+    rng = np.random.default_rng(77)
+    lo, hi = rob.limits[:, 0], rob.limits[:, 1]
+    starts = rng.uniform(lo, hi, size=(160, rob.program.dof)).astype(np.float32)
+    # short edges so some of them are collision-free in this cluttered scene
+    goals = np.clip(starts + rng.normal(0, 0.15, size=starts.shape), lo, hi).astype(np.float32)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env)
+    res = 1.0 / 32.0
+    got = runtime.unpack_bits(M.validate_motions(ctx, starts, goals, res).cpu().numpy(), len(starts))
+    expect = _edge_oracle(rob.program, rob.pairs, env.primitives, starts, goals, res)
+    assert got.tolist() == expect.tolist()
+    assert 0 < expect.sum() < len(expect)
+
+
+def _big_scene(n_prims: int):
+    return workloads.mixed_scene(900, n_prims // 2, n_prims // 4, n_prims - n_prims // 2 - n_prims // 4,
+                                 workloads.BOX_CFG1, 0.6, "big")
+
+
+def test_unstaged_environment_vs_oracle(cuda):
+    """> 96 KB of records: the kernels read obstacles from global memory."""
+    torch = cuda
+    rob = load_robot("arm7")
+    env = _big_scene(2048)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env)
+    assert ctx.device_env.bytes > 96 * 1024
+    q = workloads.uniform_configs(rob.limits, 16384, 91)
+    qd = torch.from_numpy(q).cuda()
+    for kw in ({}, {"early_exit": False}, {"split": False}):
+        words = runtime.validate_device(ctx.module, ctx.device_env, qd, q.shape[1], q.shape[1], **kw)
+        got = runtime.unpack_bits(words.cpu().numpy(), q.shape[1])
+        _parity(rob.program, rob.pairs, env.primitives, q, got, max_band=4)
+    rng = np.random.default_rng(92)
+    lo, hi = rob.limits[:, 0], rob.limits[:, 1]
+    starts = rng.uniform(lo, hi, size=(64, rob.program.dof)).astype(np.float32)
+    goals = np.clip(starts + rng.normal(0, 0.1, size=starts.shape), lo, hi).astype(np.float32)
+    got = runtime.unpack_bits(M.validate_motions(ctx, starts, goals, 1 / 32).cpu().numpy(), 64)
+    assert got.tolist() == _edge_oracle(rob.program, rob.pairs, env.primitives, starts, goals,
+                                        1 / 32).tolist()
+
+
+def test_many_sphere_scene_dense_equals_product(cuda):
+    """A 1,024-sphere scene (the old small_scene rule ignored spheres)."""
+    torch = cuda
+    rob = load_robot("arm7")
+    env = workloads.mixed_scene(901, 0, 0, 1024, workloads.BOX_CFG1, 0.6, "spheres1024")
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, env)
+    q = workloads.uniform_configs(rob.limits, 1 << 18, 93)
+    qd = torch.from_numpy(q).cuda()
+    prod = ctx.validate_batch(qd).cpu().numpy()
+    assert np.array_equal(prod, ctx.validate_batch(qd, early_exit=False).cpu().numpy())
+    got = runtime.unpack_bits(prod, q.shape[1])[:8192]
+    _parity(rob.program, rob.pairs, env.primitives, q[:, :8192], got, max_band=4)
+
+
+# --------------------------------------------------------- translated scenes
+
+OFFSETS = [d * np.array([1.0, -0.5, 0.25]) / np.linalg.norm([1.0, -0.5, 0.25])
+           for d in (5.0, 10.0, 30.0)]
+
+
+@pytest.mark.parametrize("k", range(len(OFFSETS)))
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg3", "cfg5_128"])
+def test_translated_scene_verdicts(cuda, cfg, k):
+    off = OFFSETS[k]
+    n = 16384
+    wl = {"cfg1": lambda: workloads.config1(n), "cfg3": lambda: workloads.config3(n),
+          "cfg5_128": lambda: workloads.config5(n, 128)}[cfg]()
+    rob = load_robot(wl.robot)
+    prog = translate_program(rob.program, off)
+    env = translate_env(wl.env, off)
+    ctx = ValidationContext(prog, rob.model, rob.pairs, env)
+    assert np.linalg.norm(np.asarray(ctx.device_env.origin) - off) < 2.0   # frame near the robot
+    for early in (True, False):
+        got = runtime.unpack_bits(ctx.validate_batch(wl.q, early_exit=early).cpu().numpy(), n)
+        _parity(prog, rob.pairs, env.primitives, wl.q, got, max_band=max(4, n // 2000))
+    # FK itself stays within 1e-5 m of float64 in world coordinates
+    cen = runtime.fk_spheres(prog, wl.q[:, :4096]).cpu().numpy().reshape(-1, 3, 4096)
+    ref = O.marker_centres(prog, O.rows_f64(prog, wl.q[:, :4096]))
+    assert np.max(np.abs(cen - ref)) <= 1e-5
+
+
+@pytest.mark.parametrize("k", range(len(OFFSETS)))
+def test_translated_scene_motions(cuda, k):
+    off = OFFSETS[k]
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    prog = translate_program(rob.program, off)
+    env = translate_env(mw.env, off)
+    ctx = ValidationContext(prog, rob.model, rob.pairs, env)
+    idx = np.arange(0, len(mw.starts), 16)
+    s, g = mw.starts[idx], mw.goals[idx]
+    got = runtime.unpack_bits(M.validate_motions(ctx, s, g, mw.resolution).cpu().numpy(), len(idx))
+    expect = _edge_oracle(prog, rob.pairs, env.primitives, s, g, mw.resolution)
+    assert got.tolist() == expect.tolist()
+
+
+def test_translated_lane_wrappers(cuda):
+    """Single-obstacle wrappers far from the origin (frame centred on the primitive)."""
+    from paper_2309_14545_b200 import (BoxObstacle, CapsuleObstacle, SphereObstacle,
+                                       sphere_vs_capsule_lanes, sphere_vs_cuboid_lanes,
+                                       sphere_vs_sphere_lanes)
+    rng = np.random.default_rng(8)
+    off = OFFSETS[-1]
+    rot = workloads.quat_to_matrix(rng.normal(size=4))
+    obs = [SphereObstacle(center=off + [0.1, 0, 0], radius=0.2),
+           CapsuleObstacle(p0=off - [0.2, 0, 0.1], p1=off + [0.3, 0.1, 0], radius=0.05),
+           BoxObstacle(center=off, half_extents=np.array([0.2, 0.1, 0.3]), rotation=rot)]
+    pts = (off[:, None] + rng.uniform(-0.6, 0.6, size=(3, 20000))).astype(np.float32)
+    r = 0.07
+    for ob, fn in zip(obs, (sphere_vs_sphere_lanes, sphere_vs_capsule_lanes, sphere_vs_cuboid_lanes)):
+        got = fn(pts[0], pts[1], pts[2], r, ob)
+        ref = [h for h in O.kind_hits(O.Obstacles([ob]), pts, r) if h is not None][0][0]
+        gap = O.primitive_gap_f64(ob, pts.astype(np.float64), float(np.float32(r)))
+        outside = np.abs(gap) > BAND
+        assert np.array_equal(got[outside], ref[outside])
+        assert 0 < ref.sum() < ref.size
+
+
+# ------------------------------------------------------------ workspace reuse
+
+def test_workspace_reused_across_sizes(cuda):
+    torch = cuda
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    fresh = {n: runtime.unpack_bits(M.validate_motions(ctx, mw.starts[:n], mw.goals[:n],
+                                                        mw.resolution).cpu().numpy(), n)
+             for n in (100, 4096, 37)}
+    ws = runtime.motion_workspace(4096)
+    for n in (100, 4096, 37, 4096, 100):
+        got = M.validate_motions(ctx, mw.starts[:n], mw.goals[:n], mw.resolution, workspace=ws)
+        assert runtime.unpack_bits(got.cpu().numpy(), n).tolist() == fresh[n].tolist(), n
+    # queue counters left dirty (e.g. by an aborted call): each call resets them
+    hdr = ws.view(torch.int64)
+    hdr[: 16 * 16] = 12345
+    got = M.validate_motions(ctx, mw.starts, mw.goals, mw.resolution, workspace=ws)
+    assert runtime.unpack_bits(got.cpu().numpy(), 4096).tolist() == fresh[4096].tolist()
