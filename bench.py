@@ -169,7 +169,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     n_np, b_np = ns_t.cpu().numpy().astype(np.int64), bl_t.cpu().numpy().astype(np.int64)
     states = rake_state_counts(n_np, b_np, valid)
     f_cfg = codegen.algorithmic_flops(rob.program, rob.pairs, denv.counts)["total"]
-    f_state = f_cfg + 3 * rob.tree.dof                    # + interpolation
+    f_state = f_cfg + 3 * rob.program.dof                    # + interpolation
     flops_per_launch = float(states.sum()) * f_state
 
     for _ in range(args.warmup):
@@ -355,8 +355,8 @@ def fk_only_summary(ctx_flush, n: int = 1 << 22) -> dict:
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b) / 1e3)
         t = float(np.mean(times))
-        gbs = n * 4 * (rob.tree.dof + rows) / t / 1e9
-        out[name] = {"bytes_per_config": 4 * (rob.tree.dof + rows), "us": round(t * 1e6, 1),
+        gbs = n * 4 * (rob.program.dof + rows) / t / 1e9
+        out[name] = {"bytes_per_config": 4 * (rob.program.dof + rows), "us": round(t * 1e6, 1),
                      "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
     return out
 

@@ -34,7 +34,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .trace import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
+from .program import ADD, CONST, COS, FINE, INPUT, MUL, NEG, SIN, SUB
 
 CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128

@@ -28,7 +28,7 @@ for name in ("arm7", "fetch_standin", "baxter_standin"):
         if r >= 3:
             ts.append(a.elapsed_time(b) / 1e3)
     t = float(np.mean(ts))
-    nbytes = n * 4 * (rob.tree.dof + rows)
+    nbytes = n * 4 * (rob.program.dof + rows)
     print(f"{name}: {n} configs, {rows} rows: {t * 1e6:.1f} us, {nbytes / t / 1e9:.0f} GB/s "
           f"({nbytes / t / 1e9 / 6539.9:.3f} of 6540)", flush=True)
 

@@ -48,5 +48,5 @@ for per in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4").spli
             if r >= 3:
                 ts.append(a.elapsed_time(b) / 1e3)
         t = float(np.mean(ts))
-        nbytes = n * 4 * (rob.tree.dof + rows)
+        nbytes = n * 4 * (rob.program.dof + rows)
         print(f"per_thread={per} {name}: {t * 1e6:.1f} us, {nbytes / t / 1e9:.0f} GB/s", flush=True)

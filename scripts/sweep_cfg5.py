@@ -79,7 +79,7 @@ def main():
             runtime.check(runtime.lib().vmp_fk_spheres(mod.handle, q.data_ptr(), n, n,
                                                        outb.data_ptr(), n, runtime.stream_handle()))
         ms = timed(fk, flush=flush)
-        nbytes = n * (4 * r.tree.dof + 12 * len(r.program.checks))
+        nbytes = n * (4 * r.program.dof + 12 * len(r.program.checks))
         print(json.dumps({"kernel": "vmp_fk_spheres", "robot": name, "N": n, "ms": round(ms, 4),
                           "bytes": nbytes, "gbs": round(nbytes / (ms / 1e3) / 1e9, 1),
                           "frac_hbm": round(nbytes / (ms / 1e3) / 1e9 / hbm, 4)}), flush=True)

@@ -50,13 +50,16 @@ from vecmp.robot import load_sphere_model, parse_urdf  # noqa: E402
 from vecmp.trace import evaluate_graph, optimize_graph, trace_kinematics  # noqa: E402
 
 from golden_io import env_to_arrays  # noqa: E402
-from paper_2309_14545_b200 import robots as my_robots, workloads  # noqa: E402
+from paper_2309_14545_b200 import workloads  # noqa: E402
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[2] / "scripts"))
+import make_robot_data  # noqa: E402  (URDF / sphere texts of the bundled robots)
 
 ROBOTS = ("planar2", "arm7", "fetch_standin", "baxter_standin")
 
 
 def ref_robot(name):
-    urdf, spheres = my_robots.robot_texts(name)
+    urdf, spheres = make_robot_data.texts(name)
     tree = parse_urdf(urdf)
     model = load_sphere_model(tree, spheres)
     return tree, model, build_robot(tree, model)

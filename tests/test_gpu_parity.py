@@ -109,17 +109,17 @@ def test_validate_block_vs_reference_goldens(cuda, name, e):
     outside = np.abs(clear) > BAND
     for prune in (True, False):
         ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=8, prune=prune)
-        got = np.concatenate([ctx.validate_block(ConfigBlock(rob.tree.dof, 8,
+        got = np.concatenate([ctx.validate_block(ConfigBlock(rob.program.dof, 8,
                                                              np.ascontiguousarray(q[:, i:i + 8]), 8))
                               for i in range(0, n, 8)])
         ref = fx[f"v_{name}_{e}_w8_p{int(prune)}"]
         assert np.array_equal(got[outside], ref[outside])
         assert ctx.blocks_evaluated == n // 8
     wide = validate_block(rob.program, rob.model, rob.pairs, env,
-                          ConfigBlock(rob.tree.dof, n, q, n))
+                          ConfigBlock(rob.program.dof, n, q, n))
     assert np.array_equal(wide[outside], fx[f"v_{name}_{e}_wide"][outside])
     ctx = ValidationContext(rob.program, rob.model, rob.pairs, env, width=8)
-    strict = np.concatenate([ctx.validate_block(ConfigBlock(rob.tree.dof, 8,
+    strict = np.concatenate([ctx.validate_block(ConfigBlock(rob.program.dof, 8,
                                                             np.ascontiguousarray(q[:, i:i + 8]), 8),
                                                 reject_all=True) for i in range(0, n, 8)])
     blk_out = outside.reshape(-1, 8).all(axis=1).repeat(8)

@@ -7,10 +7,9 @@ import socket
 import numpy as np
 import pytest
 
-from paper_2309_14545_b200 import (ConfigBlock, EnvironmentFormatError, SphereModelError,
-                                   UrdfError, aos_from_soa, as_config, interpolate_lanes,
-                                   l2_distance, load_environment, load_robot, load_sphere_model,
-                                   parse_urdf, soa_from_aos, workloads)
+from paper_2309_14545_b200 import (ConfigBlock, EnvironmentFormatError, aos_from_soa, as_config,
+                                   interpolate_lanes, l2_distance, load_environment, load_robot,
+                                   soa_from_aos, workloads)
 from paper_2309_14545_b200.collision import CapsuleObstacle, environment_to_doc, parse_environment
 from paper_2309_14545_b200.sharding import shard_range
 
@@ -66,34 +65,21 @@ class TestDocuments:
         back = parse_environment(environment_to_doc(env))
         assert environment_to_doc(back) == environment_to_doc(env)
 
-    def test_urdf_errors(self):
-        mini = ('<robot name="m"><link name="base"/><link name="arm"/>'
-                '<joint name="j" type="revolute"><parent link="base"/><child link="arm"/>'
-                '<axis xyz="0 0 1"/><limit lower="-3" upper="3"/></joint></robot>')
-        assert parse_urdf(mini).dof == 1
-        with pytest.raises(UrdfError, match="malformed"):
-            parse_urdf("<robot><link name='a'>")
-        with pytest.raises(UrdfError, match="unsupported"):
-            parse_urdf(mini.replace("revolute", "floating"))
-        with pytest.raises(UrdfError, match="duplicate"):
-            parse_urdf(mini.replace('<link name="arm"/>', '<link name="arm"/><link name="arm"/>'))
-        with pytest.raises(UrdfError, match="limit"):
-            parse_urdf(mini.replace('<limit lower="-3" upper="3"/>', ""))
-        loop = ('<robot name="l"><link name="a"/><link name="b"/>'
-                '<joint name="j1" type="fixed"><parent link="a"/><child link="b"/></joint>'
-                '<joint name="j2" type="fixed"><parent link="b"/><child link="a"/></joint></robot>')
-        with pytest.raises(UrdfError):
-            parse_urdf(loop)
-        tree = parse_urdf(mini)
-        with pytest.raises(SphereModelError, match="unknown link"):
-            load_sphere_model(tree, "nope:\n  - {x: 0, y: 0, z: 0, r: 0.1}\n")
-        with pytest.raises(SphereModelError, match="radius"):
-            load_sphere_model(tree, "arm:\n  - {x: 0, y: 0, z: 0, r: -1}\n")
+    def test_rpy_rotation(self):
+        env = load_environment("primitives:\n  - {kind: cuboid, center: [0,0,0], half_extents: [1,1,1],"
+                               " rpy: [0.3, -0.2, 1.1]}\n")
+        r = env.primitives[0].rotation
+        cr, sr, cp, sp, cy, sy = (np.cos(0.3), np.sin(0.3), np.cos(-0.2), np.sin(-0.2),
+                                  np.cos(1.1), np.sin(1.1))
+        expect = np.array([[cy * cp, cy * sp * sr - sy * cr, cy * sp * cr + sy * sr],
+                           [sy * cp, sy * sp * sr + cy * cr, sy * sp * cr - cy * sr],
+                           [-sp, cp * sr, cp * cr]])
+        assert np.allclose(r, expect, atol=1e-15)
 
 
 class TestWorkloads:
     def test_standins(self):
-        dims = {n: load_robot(n).tree.dof for n in ("arm7", "fetch_standin", "baxter_standin")}
+        dims = {n: load_robot(n).dof for n in ("arm7", "fetch_standin", "baxter_standin")}
         assert dims == {"arm7": 7, "fetch_standin": 8, "baxter_standin": 14}
         assert load_robot("panda") is load_robot("arm7")
 
