@@ -80,15 +80,21 @@ void vmp_robot_destroy(vmp_robot *robot);
 int vmp_env_create(const double *spheres, int32_t n_spheres, const double *capsules,
                    int32_t n_capsules, const double *boxes, int32_t n_boxes, vmp_env **out);
 /* Same, with the records expressed in a frame centred at `origin` (3 doubles,
- * rounded to float32; NULL = world origin).  Kernels subtract the origin from
- * every sphere centre before the environment tests, so with an origin near the
- * robot the expanded test forms never cancel |c|^2-sized terms (a robot 30 m
- * from the world origin keeps the same accuracy as one at the origin).
- * Verdict semantics are unchanged (reference collision.py:206-254). */
+ * rounded to float32; NULL = world origin).  vmp_validate and
+ * vmp_validate_motions need the frame of the robot they run with,
+ * vmp_robot_home(): its generated kernels test sphere centres minus that point
+ * (folded into the forward kinematics at codegen time), so the expanded test
+ * forms never cancel |c|^2-sized terms - a robot 30 m from the world origin
+ * keeps the accuracy of one at the origin.  vmp_sphere_hits subtracts the
+ * origin itself and accepts any frame.  Verdict semantics are unchanged
+ * (reference collision.py:206-254). */
 int vmp_env_create_at(const double *spheres, int32_t n_spheres, const double *capsules,
                       int32_t n_capsules, const double *boxes, int32_t n_boxes,
                       const double *origin, vmp_env **out);
 void vmp_env_destroy(vmp_env *env);
+/* The environment frame origin the robot's collision kernels assume: the mean
+ * sphere centre at the zero configuration, rounded to 1/64 m (3 doubles). */
+int vmp_robot_home(const vmp_robot *robot, double *home);
 /* Bytes of the packed device records (shared-memory staging size). */
 int64_t vmp_env_bytes(const vmp_env *env);
 

@@ -45,7 +45,7 @@ EXPORTS = (
     "vmp_fk_spheres",
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
-    "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace",
+    "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace", "vmp_robot_home",
 )
 VMP_KNN_MAX_K = 32
 VMP_KNN_MAX_DIM = 64
@@ -104,6 +104,7 @@ def lib() -> ctypes.CDLL:
         "vmp_env_create_at": ([vp, c_i32, vp, c_i32, vp, c_i32, vp, ctypes.POINTER(vp)],
                               ctypes.c_int),
         "vmp_env_destroy": ([vp], None),
+        "vmp_robot_home": ([vp, vp], ctypes.c_int),
         "vmp_env_bytes": ([vp], c_i64),
         "vmp_fk_rows": ([vp, vp, c_i64, c_i64, vp, c_i64, vp], ctypes.c_int),
         "vmp_fk_spheres": ([vp, vp, c_i64, c_i64, vp, c_i64, vp], ctypes.c_int),

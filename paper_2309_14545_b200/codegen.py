@@ -58,7 +58,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 27
+CODEGEN_VERSION = 28
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
 # this before codegen runs); off in production - they cost ~2 % of the step
 TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
@@ -96,6 +96,7 @@ class RobotLayout:
     pairs: tuple       # (slot_a, slot_b, thr_f32)
     has_cc: bool       # pairs given -> collision kernels emitted
     link_pairs: frozenset = frozenset()   # checked (lo, hi) link pairs
+    home: tuple = (0.0, 0.0, 0.0)         # environment frame origin (robot_home)
 
     @property
     def dynamic(self) -> list:
@@ -134,7 +135,8 @@ def derive_layout(program, pairs=None) -> RobotLayout:
                        fine=tuple(fine), coarse=coarse, pairs=tuple(pair_list),
                        has_cc=pairs is not None,
                        link_pairs=frozenset(tuple(sorted(p)) for p in pairs.pairs)
-                       if pairs is not None else frozenset())
+                       if pairs is not None else frozenset(),
+                       home=robot_home(program))
 
 
 def _fk_lines(program) -> list[str]:
@@ -181,36 +183,108 @@ def _xyz(s: FineSphere) -> tuple[str, str, str]:
     return tuple(f"v{v}" for v in s.xyz)
 
 
-def _exyz(s: FineSphere) -> tuple[str, str, str]:
-    """Centre of a dynamic sphere in the environment's frame (minus its origin)."""
-    return tuple(f"E{s.slot}{axis}" for axis in "xyz")
+def _values_at_zero(program) -> np.ndarray:
+    """float64 value of every op at the zero configuration (codegen-time
+    analysis only: the home point and the operand choice of ``_HomeShift``)."""
+    kinds, a, b, values = program.kinds, program.a, program.b, program.values
+    val = np.zeros(len(kinds))
+    for i, k in enumerate(int(k) for k in kinds):
+        x = val[a[i]] if a[i] >= 0 else 0.0
+        y = val[b[i]] if b[i] >= 0 else 0.0
+        val[i] = {CONST: values[i], INPUT: 0.0, ADD: x + y, SUB: x - y, MUL: x * y, NEG: -x,
+                  SIN: np.sin(x), COS: np.cos(x)}[k]
+    return val
 
 
-def _state_function(lay: RobotLayout) -> str:
+def robot_home(program) -> tuple:
+    """Origin of the environment frame the collision kernels work in: the mean
+    sphere centre at the zero configuration, rounded to 1/64 m (exact in
+    float32).  Obstacle records are packed relative to it (vmp_env_create_at),
+    so the expanded test forms (|c|^2 + |o|^2 - 2 c.o) never cancel
+    |c|^2-sized terms for a robot far from the world origin."""
+    if not program.checks:
+        return (0.0, 0.0, 0.0)
+    val = _values_at_zero(program)
+    c = np.asarray([[val[v] for v in m.xyz] for m in program.checks]).mean(axis=0)
+    return tuple(float(v) for v in np.round(c * 64.0) / 64.0)
+
+
+class _HomeShift:
+    """Sphere-centre coordinates minus the home point, folded into the op DAG.
+
+    shift(op, axis) is an expression for value(op) - home[axis]: a CONST op
+    folds to a new literal; ADD / SUB move the subtraction into the operand
+    that carries the translation (the one nearer home at the zero
+    configuration), so along the usual translation chains no operation is
+    added - the rewritten sums replace the originals, which become dead; any
+    other op gets one FADD.  Errors stay linear in |home| (one rounding of a
+    value near home), unlike the quadratic cancellation of the expanded forms.
+    """
+
+    def __init__(self, program, home):
+        self.kinds = [int(k) for k in program.kinds]
+        self.a = [int(x) for x in program.a]
+        self.b = [int(x) for x in program.b]
+        self.values = [float(v) for v in program.values]
+        self.home = home
+        self.val = _values_at_zero(program) if any(home) else None
+        self.memo: dict = {}
+        self.lines: list[str] = []
+
+    def __call__(self, op: int, axis: int) -> str:
+        o = self.home[axis]
+        if o == 0.0:
+            return f"v{op}"
+        key = (op, axis)
+        if key in self.memo:
+            return self.memo[key]
+        k = self.kinds[op]
+        if k == CONST:
+            expr = f32_literal(self.values[op] - o)
+        else:
+            if k == ADD:
+                x, y = self.a[op], self.b[op]
+                if abs(self.val[y] - o) < abs(self.val[x] - o):
+                    x, y = y, x
+                rhs = f"{self(x, axis)} + v{y}"
+            elif k == SUB:
+                rhs = f"{self(self.a[op], axis)} - v{self.b[op]}"
+            else:
+                rhs = f"v{op} - {f32_literal(o)}"
+            expr = f"h{len(self.lines)}"
+            self.lines.append(f"  const float {expr} = {rhs};")
+        self.memo[key] = expr
+        return expr
+
+    def xyz(self, ops) -> tuple[str, str, str]:
+        return tuple(self(int(v), axis) for axis, v in enumerate(ops))
+
+
+def _state_function(lay: RobotLayout, program) -> str:
     dyn = lay.dynamic
     out = []
     emit = out.append
     emit("template <int STOP, bool PRUNE, bool TWO = (STOP == 2), bool NO_SPH = false>")
     emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
-    emit("                                          int ns, int nc, int nb, float3 org, bool ok,")
+    emit("                                          int ns, int nc, int nb, bool ok,")
     emit("                                          int sub = 0, int split = 1,")
     emit("                                          unsigned long long *bar = nullptr) {")
     emit("  // split > 1: this thread handles obstacles k = sub (mod split) and self")
     emit("  // pairs i = sub (mod split) of its configuration (small-batch kernels)")
-    emit("  (void)env; (void)ns; (void)nc; (void)nb; (void)org;")
+    emit("  (void)env; (void)ns; (void)nc; (void)nb;")
     for line in _FK_BODY_PLACEHOLDER:
         emit(line)
-    # environment tests run in the environment's frame: centres minus the
-    # env origin (records are packed relative to it), so the expanded test
-    # forms never cancel |c|^2-sized terms for a robot far from the world
-    # origin; self pairs and group radii use differences and stay in world
-    # coordinates
-    for s in lay.dynamic:
-        for axis, v in zip("xyz", s.xyz):
-            emit(f"  const float E{s.slot}{axis} = v{v} - org.{axis};")
-    for link, (_, xyz) in lay.coarse.items():
-        for axis, v in zip("xyz", xyz):
-            emit(f"  const float K{link}{axis} = v{v} - org.{axis};")
+    # every collision test runs in the environment frame centred at the robot's
+    # home point (obstacle records are packed relative to it): sphere centres
+    # minus home, folded into the FK sums (_HomeShift) - no per-state cost
+    shift = _HomeShift(program, lay.home)
+    env_xyz = {s.slot: shift.xyz(s.xyz) for s in lay.fine}
+    coarse_env = {link: shift.xyz(xyz) for link, (_, xyz) in lay.coarse.items()}
+    for line in shift.lines:
+        emit(line)
+
+    def _exyz(s: FineSphere) -> tuple[str, str, str]:
+        return env_xyz[s.slot]
     emit("#define VMP_STOP_NOW ((STOP == 1 && !__any_sync(VMP_FULL, ok)) || "
          "(STOP == 2 && __any_sync(VMP_FULL, !ok && vmp_inr)))")
     emit("  const bool vmp_inr = ok;")
@@ -225,8 +299,8 @@ def _state_function(lay: RobotLayout) -> str:
     emit("  constexpr bool CULL_SELF = STOP == 2;")
     emit("  if constexpr (!CULL_SELF) {")
     for pi, (sa, sb, thr) in enumerate(lay.pairs):
-        ax, ay, az = _xyz(fine[sa])
-        bx, by, bz = _xyz(fine[sb])
+        ax, ay, az = _exyz(fine[sa])
+        bx, by, bz = _exyz(fine[sb])
         emit(f"    if (sub == {pi} % split) "
              f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
     emit("  }")
@@ -242,12 +316,12 @@ def _state_function(lay: RobotLayout) -> str:
     emit("  constexpr bool CULL = STOP != 0;")
     for gi, grp in enumerate(groups):
         mid = grp[len(grp) // 2]
-        mx, my, mz = _xyz(mid)
+        mx, my, mz = _exyz(mid)
         emit(f"  float G{gi}R = {f32_literal(mid.radius)};")
         for s in grp:
             if s is mid:
                 continue
-            x, y, z = _xyz(s)
+            x, y, z = _exyz(s)
             emit(f"  G{gi}R = fmaxf(G{gi}R, vmp_dist({x}, {y}, {z}, {mx}, {my}, {mz}) + "
                  f"{f32_literal(s.radius)});")
         emit(f"  G{gi}R = fmaf(G{gi}R, 1.000002f, 1e-6f);")
@@ -264,12 +338,12 @@ def _state_function(lay: RobotLayout) -> str:
     group_of: dict[int, tuple] = {}
     links_of: dict[str, set] = {}
     for gi, grp in enumerate(groups):
-        mxyz = _xyz(grp[len(grp) // 2])
+        mxyz = _exyz(grp[len(grp) // 2])
         for s in grp:
             group_of[s.slot] = (f"g{gi:03d}", mxyz, f"G{gi}R")
             links_of.setdefault(f"g{gi:03d}", set()).add(s.link)
     for s in lay.const_spheres:
-        group_of[s.slot] = (f"c{s.slot:03d}", _xyz(s), f32_literal(s.radius))
+        group_of[s.slot] = (f"c{s.slot:03d}", _exyz(s), f32_literal(s.radius))
         links_of.setdefault(f"c{s.slot:03d}", set()).add(s.link)
 
     def touching(ka, kb):
@@ -285,8 +359,8 @@ def _state_function(lay: RobotLayout) -> str:
     for (ka, kb), items in buckets.items():
         tests = []
         for sa, sb, thr in items:
-            ax, ay, az = _xyz(fine[sa])
-            bx, by, bz = _xyz(fine[sb])
+            ax, ay, az = _exyz(fine[sa])
+            bx, by, bz = _exyz(fine[sb])
             tests.append(f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, "
                          f"{f32_literal(thr)}); ")
         if ka == kb or (ka[0] == "c" and kb[0] == "c") or touching(ka, kb):
@@ -319,8 +393,7 @@ def _state_function(lay: RobotLayout) -> str:
                     emit(ind + "ok &= " + t + ";")
 
     def coarse_xyz(link):
-        r, _ = lay.coarse[link]
-        return r, tuple(f"K{link}{axis}" for axis in "xyz")
+        return lay.coarse[link][0], coarse_env[link]
 
     def sph_test(s):
         x, y, z = _exyz(s)
@@ -445,9 +518,8 @@ _FK_BODY_PLACEHOLDER = ["  VMP_FK_BODY"]
 def _const_check(lay: RobotLayout) -> str:
     """Per-CTA test of configuration-independent spheres against the env."""
     consts = lay.const_spheres
-    lines = ["__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb,",
-             "                                                float3 org) {",
-             "  (void)env; (void)ns; (void)nc; (void)nb; (void)org;",
+    lines = ["__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb) {",
+             "  (void)env; (void)ns; (void)nc; (void)nb;",
              "  bool ok = true;"]
     if consts:
         # (const sphere, obstacle) pairs spread over the CTA's threads
@@ -458,8 +530,7 @@ def _const_check(lay: RobotLayout) -> str:
         for k, s in enumerate(consts):
             # centre coordinates of a const sphere are CONST ops: exact float32 literals
             lines.append(f"    case {k}: ok &= vmp_sphere_clear_obstacle(env, ns, nc, nb, k, "
-                         f"VMP_C{s.slot}X - org.x, VMP_C{s.slot}Y - org.y, VMP_C{s.slot}Z - org.z, "
-                         f"{f32_literal(s.radius)}); break;")
+                         f"VMP_C{s.slot}X, VMP_C{s.slot}Y, VMP_C{s.slot}Z, {f32_literal(s.radius)}); break;")
         lines.append("    default: break;")
         lines.append("    }")
         lines.append("  }")
@@ -589,7 +660,6 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   // the environment copy overlaps the joint loads, FK and self pairs of the
   // first tile; vmp_state waits for it before the first obstacle
   const float4 *env = STAGED ? vmp_smem : a.env.rec;
-  const float3 org = make_float3(a.env.ox, a.env.oy, a.env.oz);
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
     __syncthreads();
@@ -604,11 +674,11 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
     const long long ii = inr ? i : a.n - 1;
     float q[{dofp}];
 {ld_q}
-    bool ok = vmp_state<STOP, PRUNE != 0, TWO>(q, env, a.env.ns, a.env.nc, a.env.nb, org, inr, sub,
+    bool ok = vmp_state<STOP, PRUNE != 0, TWO>(q, env, a.env.ns, a.env.nc, a.env.nb, inr, sub,
                                                SPLIT, STAGED ? &vmp_bar : nullptr);
     if (!cdone) {{                            // CTA-uniform: once, after the first tile
       if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
-      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, org));
+      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
       cdone = true;
     }}
     ok = ok && cclear;
@@ -652,14 +722,13 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // retire and wait (griddepcontrol.wait) for this whole grid
   asm volatile("griddepcontrol.launch_dependents;");
   const float4 *env = a.env.rec;
-  const float3 org = make_float3(a.env.ox, a.env.oy, a.env.oz);
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
     __syncthreads();
     vmp_mbar_wait(&vmp_bar, 0);
     env = vmp_smem;
   }}
-  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, org));
+  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
   if (trace && threadIdx.x == 0) trace[1] = vmp_gtime();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long E = a.n_edges;
@@ -765,7 +834,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
 #pragma unroll
       for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
       const bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc,
-                                                                  a.env.nb, org, inr && cclear);
+                                                                  a.env.nb, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
       if (bad && lane == 0) {{
         const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
@@ -819,9 +888,12 @@ def generate_source(program, pairs=None, name: str = "robot") -> str:
     fk_macro = " \\\n  ".join(fk) if fk else ""
     const_defs = []
     values = np.asarray(program.values)
-    for s in lay.const_spheres:
-        for axis, op in zip("XYZ", s.xyz):
-            const_defs.append(f"#define VMP_C{s.slot}{axis} {f32_literal(values[op])}")
+    for s in lay.const_spheres:          # constant centres, in the environment frame
+        for axis, op, o in zip("XYZ", s.xyz, lay.home):
+            const_defs.append(f"#define VMP_C{s.slot}{axis} {f32_literal(values[op] - o)}")
+    # the environment frame the collision kernels assume (read by vmp_robot_load)
+    const_defs.append('extern "C" __device__ const float vmp_home[3] = {'
+                      + ", ".join(f32_literal(o) for o in lay.home) + "};")
     parts = [
         f"// generated by paper_2309_14545_b200.codegen v{CODEGEN_VERSION}",
         f"// dof={lay.dof} ops={lay.n_ops} markers={lay.n_markers} fine={len(lay.fine)} "
@@ -832,7 +904,7 @@ def generate_source(program, pairs=None, name: str = "robot") -> str:
     ]
     if lay.has_cc:
         parts.append(_const_check(lay))
-        parts.append(_state_function(lay))
+        parts.append(_state_function(lay, program))
     parts.append(_kernels(lay, program))
     return "\n".join(parts) + "\n"
 

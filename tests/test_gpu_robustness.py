@@ -229,3 +229,20 @@ def test_workspace_reused_across_sizes(cuda):
     hdr[: 16 * 16] = 12345
     got = M.validate_motions(ctx, mw.starts, mw.goals, mw.resolution, workspace=ws)
     assert runtime.unpack_bits(got.cpu().numpy(), 4096).tolist() == fresh[4096].tolist()
+
+
+def test_environment_frame_must_match_robot_home(cuda):
+    """The generated kernels assume obstacles packed relative to the robot's
+    home point; the library rejects an environment packed in another frame."""
+    torch = cuda
+    rob = load_robot("arm7")
+    wl = workloads.config1(64)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    assert ctx.device_env.origin == ctx.module.home != (0.0, 0.0, 0.0)
+    world = runtime.DeviceEnv(wl.env.primitives, origin=(0.0, 0.0, 0.0))
+    qd = torch.from_numpy(wl.q).cuda()
+    with pytest.raises(ValueError, match="frame"):
+        runtime.validate_device(ctx.module, world, qd, 64, 64)
+    with pytest.raises(ValueError, match="frame"):
+        runtime.validate_motions_device(ctx.module, world, qd.T.contiguous()[:4],
+                                        qd.T.contiguous()[4:8], 1 / 32)
