@@ -144,6 +144,19 @@ int64_t vmp_motion_workspace_bytes(int64_t n_edges);
 int vmp_discretize(const float *starts, const float *goals, int64_t n_edges, int32_t dim,
                    int64_t sld, double resolution, int32_t *n_out, void *stream);
 
+/* The states the rake visits (reference motion.py:32-78 strata,
+ * lanes.py:91-103 interpolate_lanes), written in the rake kernels' position
+ * order with the same device arithmetic, for parity checks and callers that
+ * want the sample points: edge e occupies positions [offsets[e],
+ * offsets[e] + S_e W), S_e = ceil(n_e / W) (offsets: n_edges + 1 device int64,
+ * exclusive prefix sum the caller computes from vmp_discretize).  Position
+ * p holds index_out = k S + j (k = p mod W, j = p / W + 1; S - j + 1 with
+ * VMP_BACKWARD), or 0 past n, and the state (dim floats, row p) at
+ * t = f32(index / n) (index 1 past n). */
+int vmp_motion_states(const float *starts, const float *goals, int64_t n_edges, int32_t dim,
+                      int64_t sld, double resolution, int32_t width, uint32_t flags,
+                      const int64_t *offsets, int32_t *index_out, float *states, void *stream);
+
 /* Per-obstacle, per-lane contact of spheres of one radius against env
  * (hits: n_obstacles x n bytes, 1 = contact, obstacle order spheres,
  * capsules, boxes).  Backs sphere_vs_{sphere,capsule,cuboid}_lanes
@@ -174,7 +187,8 @@ int vmp_knn(const float *points, int64_t n_points, int64_t ld, int32_t dim, cons
             float *out_dist, void *stream);
 
 /* Every query-to-point distance (same arithmetic as vmp_knn) into out
- * (n_queries x ldo); the k > VMP_KNN_MAX_K path sorts these stably. */
+ * (n_queries x ldo), any dim in [1, 12288]; the k > VMP_KNN_MAX_K and
+ * dim > VMP_KNN_MAX_DIM paths sort these stably. */
 int vmp_nn_distances(const float *points, int64_t n_points, int64_t ld, int32_t dim,
                      const float *queries, int64_t n_queries, int64_t qld, float *out, int64_t ldo,
                      void *stream);

@@ -46,6 +46,7 @@ EXPORTS = (
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
     "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace", "vmp_robot_home",
+    "vmp_motion_states",
 )
 VMP_KNN_MAX_K = 32
 VMP_KNN_MAX_DIM = 64
@@ -113,6 +114,8 @@ def lib() -> ctypes.CDLL:
                                   vp, c_i64, vp], ctypes.c_int),
         "vmp_motion_workspace_bytes": ([c_i64], c_i64),
         "vmp_discretize": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, vp, vp], ctypes.c_int),
+        "vmp_motion_states": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, c_i32, c_u32, vp, vp, vp, vp],
+                              ctypes.c_int),
         "vmp_sphere_hits": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),
         "vmp_pair_clear": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),
         "vmp_knn": ([vp, c_i64, c_i64, c_i32, vp, c_i64, c_i64, vp, c_i32, vp, vp, vp],

@@ -10,8 +10,10 @@ next query.  ``k_nearest_many`` answers a batch of queries in one launch,
 each optionally restricted to a prefix of the index (a query issued
 "between" inserts, as the PRM round does).
 
-k <= 32 runs the warp top-k kernel (vmp_knn); larger k sorts the full
-distance row (vmp_nn_distances) with a stable device sort.
+k <= 32 (dim <= 64) runs the query-tiled top-k kernel (vmp_knn); larger k or
+dim sorts the full distance row (vmp_nn_distances, any dim up to 12,288)
+with a stable device sort - same answers, no dimension limit in practice
+(the reference's NNIndex has none).
 """
 
 from __future__ import annotations
@@ -21,13 +23,15 @@ import numpy as np
 from . import runtime
 from ._native import VMP_KNN_MAX_DIM, VMP_KNN_MAX_K
 
+NN_MAX_DIM = 12288          # vmp_nn_distances stages a query row in shared memory
+
 
 class NNIndex:
     def __init__(self, dim: int):
         if dim < 1:
             raise ValueError("dim must be >= 1")
-        if dim > VMP_KNN_MAX_DIM:
-            raise ValueError(f"dim must be <= {VMP_KNN_MAX_DIM}")
+        if dim > NN_MAX_DIM:
+            raise ValueError(f"dim must be <= {NN_MAX_DIM}")
         self.dim = dim
         self._payloads: list = []
         self._ids: set = set()
@@ -81,7 +85,7 @@ class NNIndex:
         qd = runtime.to_device(np.ascontiguousarray(qs, dtype=np.float32).reshape(-1, self.dim))
         vis = None if visible is None else torch.as_tensor(
             np.asarray(visible, dtype=np.int64)).to(qd.device)
-        if k <= VMP_KNN_MAX_K:
+        if k <= VMP_KNN_MAX_K and self.dim <= VMP_KNN_MAX_DIM:
             return runtime.knn_device(points, n, qd, k, vis)
         dist = runtime.nn_distances_device(points, n, qd)
         if vis is not None:

@@ -38,7 +38,7 @@ import numpy as np
 
 from . import runtime
 from .lanes import l2_distance
-from .motion import validate_motions
+from .motion import _bind
 
 
 @dataclass
@@ -96,12 +96,31 @@ def _point_at(waypoints, cum: np.ndarray, u: float):
     return seg, (a + t32 * (b - a)).astype(np.float32)
 
 
-def _free(ctx, starts: list, goals: list, resolution: float) -> np.ndarray:
-    """Verdicts of a batch of motions: one device launch."""
-    if not starts:
-        return np.zeros(0, dtype=bool)
-    words = validate_motions(ctx, np.stack(starts), np.stack(goals), resolution)
-    return runtime.unpack_bits(words.cpu().numpy(), len(starts))
+class _Batch:
+    """Verdicts and ctx.width-lane rake block counts of speculated motions (one
+    device launch).  The context's counters are NOT touched by the launch:
+    ``charge(i)`` adds motion i exactly as the reference's sequential
+    ``validate_motion_rake`` call would (motion.py:60 and one block per rake
+    iteration), so after the replay ``ctx.motion_checks`` /
+    ``ctx.blocks_evaluated`` equal the reference's."""
+
+    def __init__(self, ctx, starts: list, goals: list, resolution: float):
+        self.ctx = ctx
+        self.free = np.zeros(0, dtype=bool)
+        self.blocks = np.zeros(0, dtype=np.int64)
+        if starts:
+            sd = runtime.to_device(np.stack(starts))
+            gd = runtime.to_device(np.stack(goals))
+            words, _, blocks = runtime.validate_motions_device(
+                *_bind(ctx), sd, gd, resolution, width=int(getattr(ctx, "width", 8)),
+                prune=getattr(ctx, "prune", True), want_counts=True)
+            self.free = runtime.unpack_bits(words.cpu().numpy(), len(starts))
+            self.blocks = blocks.cpu().numpy().astype(np.int64)
+
+    def charge(self, i: int) -> bool:
+        self.ctx.motion_checks += 1
+        self.ctx.blocks_evaluated += int(self.blocks[i])
+        return bool(self.free[i])
 
 
 def _like(path, waypoints):
@@ -139,13 +158,14 @@ def shortcut(path, ctx, settings: SimplifySettings, *, speculate: int = 32):
             cands.append((seg1, qa, seg2, qb))
             starts += [waypoints[seg1], qa, qb]
             goals += [qa, qb, waypoints[seg2 + 1]]
-        free = _free(ctx, starts, goals, settings.resolution)
+        batch = _Batch(ctx, starts, goals, settings.resolution)
         accepted = None
         m = 0
         for k, cand in enumerate(cands):
             if cand is None:
                 continue
-            ok = bool(free[m] and free[m + 1] and free[m + 2])
+            # the reference checks the three motions in order and stops at the first failure
+            ok = batch.charge(m) and batch.charge(m + 1) and batch.charge(m + 2)
             m += 3
             if not ok:
                 continue
@@ -186,11 +206,11 @@ def _smooth_window(ctx, waypoints: list, lo: int, hi: int, resolution: float) ->
     starts = np.concatenate([np.concatenate([h, p]) for h, p, _ in steps])
     goals = np.concatenate([np.concatenate([p, np.broadcast_to(n, p.shape)])
                             for _, p, n in steps])
-    free = _free(ctx, list(starts), list(goals), resolution)
+    batch = _Batch(ctx, list(starts), list(goals), resolution)
     live = pos = 0
     for i, (_, prop, _) in zip(range(lo, hi), steps):
         n = prop.shape[0]
-        if free[pos + live] and free[pos + n + live]:
+        if batch.charge(pos + live) and batch.charge(pos + n + live):
             waypoints[i] = prop[live].copy()            # accepted: same chain continues
         else:
             live = n                                    # rejected: chain started at i

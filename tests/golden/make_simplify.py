@@ -74,12 +74,20 @@ def main() -> None:
         st = SimplifySettings(resolution=ps.settings.resolution, rng_seed=seed)
         ctx = ValidationContext(ps.robot.program, ps.robot.model, ps.robot.pairs, case.env,
                                 width=ps.settings.width)
+        counters = []
+
+        def tally():
+            counters.extend([ctx.motion_checks, ctx.blocks_evaluated])
+            ctx.motion_checks = ctx.blocks_evaluated = 0
         t0 = time.perf_counter()
         sc = shortcut(path, ctx, st)
+        tally()
         t1 = time.perf_counter()
         sm = bspline_smooth(path, ctx, st)
+        tally()
         t2 = time.perf_counter()
         both = simplify_path(path, ctx, st)
+        tally()
         kinds, params = env_to_arrays(case.env)
         out[f"env_{key}_kinds"], out[f"env_{key}_params"] = kinds, params
         out[f"settings_{key}"] = np.asarray([st.resolution, st.shortcut_attempts,
@@ -89,6 +97,10 @@ def main() -> None:
         out[f"smooth_{key}"] = np.stack(sm.waypoints)
         out[f"simplify_{key}"] = np.stack(both.waypoints)
         out[f"seconds_{key}"] = np.asarray([t1 - t0, t2 - t1])
+        # ValidationContext counters (motion_checks, blocks_evaluated) of each
+        # call: shortcut, bspline_smooth, simplify_path
+        out[f"counters_{key}"] = np.asarray(counters, dtype=np.int64)
+        out[f"width_{key}"] = np.asarray(ctx.width)
         print(f"{key}: {len(path.waypoints)} -> shortcut {len(sc.waypoints)} "
               f"({t1 - t0:.2f} s), smooth ({t2 - t1:.2f} s), "
               f"cost {path.cost:.3f} -> {both.cost:.3f}", flush=True)

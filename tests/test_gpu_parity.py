@@ -212,6 +212,77 @@ def test_block_validator_sink_matches_fused_path(cuda):
     assert len(calls) < len(rob.program.checks)
 
 
+def test_validate_block_drives_caller_sink(cuda):
+    """validate_block(..., sink=s) resets s, drives it through evaluate_program
+    and returns s.result() (reference collision.py:422-429)."""
+    from paper_2309_14545_b200 import BlockValidator
+    fx = golden_io.load("blocks")
+    rob = load_robot("arm7")
+    env = golden_io.env_from(fx, "env_arm7_4")
+    q = np.ascontiguousarray(fx["q_arm7"][:, :64])
+    outside = np.abs(O.clearance_f64(rob.program, rob.pairs, env.primitives, q)) > BAND
+    for reject_all in (False, True):
+        ref = fx[f"v_arm7_4_{'reject_all' if reject_all else 'w8_p1'}"][:64]
+        sink = BlockValidator(env.packed(), rob.pairs, width=8, reject_all=not reject_all)
+        sink.valid[:] = False                      # stale state: validate_block resets it
+        got = []
+        for i in range(0, 64, 8):
+            out = validate_block(rob.program, rob.model, rob.pairs, env,
+                                 ConfigBlock(7, 8, np.ascontiguousarray(q[:, i:i + 8]), 8),
+                                 reject_all=reject_all, sink=sink)
+            assert np.array_equal(out, sink.result()) and sink.reject_all == reject_all
+            got.append(out)
+        got = np.concatenate(got)
+        blk = outside.reshape(-1, 8).all(axis=1).repeat(8) if reject_all else outside
+        assert np.array_equal(got[blk], ref[blk])
+
+    class Recorder:                                # any object with the sink protocol
+        def __init__(self):
+            self.resets, self.calls = [], 0
+
+        def reset(self, prune=None, reject_all=None):
+            self.resets.append((prune, reject_all))
+
+        def __call__(self, marker, x, y, z):
+            self.calls += 1
+            return False
+
+        def result(self):
+            return np.full(8, True)
+
+    rec = Recorder()
+    out = validate_block(rob.program, rob.model, rob.pairs, env,
+                         ConfigBlock(7, 8, np.ascontiguousarray(q[:, :8]), 8), prune=False,
+                         sink=rec)
+    assert out.all() and rec.resets == [(False, False)] and rec.calls == len(rob.program.checks)
+
+
+@pytest.mark.parametrize("width,backward", [(32, False), (32, True), (8, False), (8, True),
+                                            (5, True), (1, False)])
+def test_rake_states_bit_exact(cuda, width, backward):
+    """Every state the rake visits (vmp_motion_states: the rake kernels' index
+    math, vmp_rake_param and vmp_lerp_exact) equals the reference's
+    interpolate_lanes at t = f32(i / n) bit for bit, in the reference's
+    stratum order (motion.py:32-78, lanes.py:91-103)."""
+    mw = workloads.config2()
+    E = 512
+    s, g = mw.starts[:E], mw.goals[:E]
+    n, off, idx, st = runtime.motion_states(runtime.to_device(s), runtime.to_device(g),
+                                            mw.resolution, width=width, backward=backward)
+    for e in range(E):
+        ne = O.discretization(s[e], g[e], mw.resolution)
+        assert n[e] == ne
+        S = -(-ne // width)
+        order = range(S, 0, -1) if backward else range(1, S + 1)
+        exp = np.concatenate([np.arange(width, dtype=np.int64) * S + j for j in order])
+        inr = exp <= ne
+        got_idx = idx[off[e]:off[e + 1]]
+        assert np.array_equal(got_idx, np.where(inr, exp, 0))
+        ref = O.rake_states(s[e], g[e], ne, exp[inr]).T
+        got = st[off[e]:off[e + 1]][inr]
+        assert np.array_equal(got.view(np.uint32), np.ascontiguousarray(ref).view(np.uint32))
+
+
 # ---------------------------------------------------------- narrowphase
 
 def test_single_obstacle_lane_wrappers_vs_reference(cuda):

@@ -76,7 +76,8 @@ def test_device_index_errors_mirror_reference(cuda):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dim,n,k", [(7, 100_000, 8), (14, 30_000, 32), (3, 5000, 64)])
+@pytest.mark.parametrize("dim,n,k", [(7, 100_000, 8), (14, 30_000, 32), (3, 5000, 64),
+                                     (100, 3000, 5), (300, 2000, 40)])
 def test_batched_prefix_queries_match_oracle(cuda, dim, n, k):
     """k_nearest_many with per-query visible prefixes == the oracle on each prefix."""
     rng = np.random.default_rng(dim * 1000 + k)

@@ -44,20 +44,38 @@ def _same(out, key, what):
 
 @pytest.fixture()
 def oracle_verdicts(monkeypatch):
-    """Replace the device batch with the oracle rake, counting batches."""
+    """Replace the device batch with the oracle rake (verdicts and ctx.width-lane
+    block counts), counting batches."""
     calls = []
 
-    def free(ctx, starts, goals, resolution):
-        calls.append(len(starts))
-        ob = O.Obstacles(ctx.env.primitives)
-        return np.asarray([O.rake_check(ctx.program, ctx.pairs, ob, s, g, resolution)[0]
-                           for s, g in zip(starts, goals)], dtype=bool)
-    monkeypatch.setattr(simplify, "_free", free)
+    class OracleBatch(simplify._Batch):
+        def __init__(self, ctx, starts, goals, resolution):
+            calls.append(len(starts))
+            self.ctx = ctx
+            ob = O.Obstacles(ctx.env.primitives)
+            res = [O.rake_check(ctx.program, ctx.pairs, ob, s, g, resolution, width=ctx.width)
+                   for s, g in zip(starts, goals)]
+            self.free = np.asarray([r[0] for r in res], dtype=bool)
+            self.blocks = np.asarray([r[1] for r in res], dtype=np.int64)
+    monkeypatch.setattr(simplify, "_Batch", OracleBatch)
     return calls
 
 
-def _host_ctx(robot, env):
-    return types.SimpleNamespace(program=robot.program, pairs=robot.pairs, env=env)
+def _host_ctx(robot, env, width=8):
+    return types.SimpleNamespace(program=robot.program, pairs=robot.pairs, env=env, width=width,
+                                 motion_checks=0, blocks_evaluated=0)
+
+
+def _counters(ctx, key, which):
+    """ctx counters == the reference's for call `which` (0 shortcut, 1 smooth, 2 simplify)."""
+    if f"counters_{key}" not in FX.files:
+        return
+    expect = FX[f"counters_{key}"][2 * which: 2 * which + 2].tolist()
+    assert [ctx.motion_checks, ctx.blocks_evaluated] == expect, (key, which)
+
+
+def _width(key):
+    return int(FX[f"width_{key}"]) if f"width_{key}" in FX.files else 8
 
 
 def test_settings_and_cost_mirror_reference():
@@ -87,24 +105,28 @@ def test_trivial_paths_are_identity(oracle_verdicts):
 @pytest.mark.parametrize("key", CPU_KEYS)
 def test_shortcut_speculation_matches_reference(oracle_verdicts, key):
     robot, env, st, path = _case(key)
-    ctx = _host_ctx(robot, env)
     for spec in (1, 7, 32):
+        ctx = _host_ctx(robot, env, _width(key))
         _same(simplify.shortcut(path, ctx, st, speculate=spec), key, "shortcut")
+        _counters(ctx, key, 0)
 
 
 @pytest.mark.parametrize("key", CPU_KEYS)
 def test_smooth_chains_match_reference(oracle_verdicts, key):
     robot, env, st, path = _case(key)
-    ctx = _host_ctx(robot, env)
     for window in (1, 5, 32):
+        ctx = _host_ctx(robot, env, _width(key))
         _same(simplify.bspline_smooth(path, ctx, st, window=window), key, "smooth")
+        _counters(ctx, key, 1)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("key", KEYS)
 def test_simplify_on_device_matches_reference(cuda, key):
     robot, env, st, path = _case(key)
-    ctx = ValidationContext(robot.program, robot.model, robot.pairs, env)
-    _same(simplify.shortcut(path, ctx, st), key, "shortcut")
-    _same(simplify.bspline_smooth(path, ctx, st), key, "smooth")
-    _same(simplify.simplify_path(path, ctx, st), key, "simplify")
+    for which, (what, fn) in enumerate((("shortcut", simplify.shortcut),
+                                        ("smooth", simplify.bspline_smooth),
+                                        ("simplify", simplify.simplify_path))):
+        ctx = ValidationContext(robot.program, robot.model, robot.pairs, env, width=_width(key))
+        _same(fn(path, ctx, st), key, what)
+        _counters(ctx, key, which)
