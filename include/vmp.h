@@ -144,6 +144,33 @@ int64_t vmp_motion_workspace_bytes(int64_t n_edges);
 int vmp_discretize(const float *starts, const float *goals, int64_t n_edges, int32_t dim,
                    int64_t sld, double resolution, int32_t *n_out, void *stream);
 
+/* Host-buffer variants of vmp_validate / vmp_validate_motions for callers
+ * with host data (the reference's per-call API: state_valid, a W = 8
+ * validate_block, one raked_motion_check): copy the inputs (host, row stride
+ * ld / sld floats; pinned memory makes the copies asynchronous DMA) into
+ * `scratch` (device, >= the *_scratch_bytes size), run the kernels, copy the
+ * verdict words (and optional per-edge n / W-lane block counts) back to host
+ * memory, and synchronise `stream` - one C call per request. */
+int64_t vmp_validate_host_scratch_bytes(const vmp_robot *robot, int64_t n);
+int vmp_validate_host(const vmp_robot *robot, const vmp_env *env, const float *q_host, int64_t n,
+                      int64_t ld, uint32_t flags, uint32_t *bits_host, void *scratch,
+                      int64_t scratch_bytes, void *stream);
+int64_t vmp_motions_host_scratch_bytes(const vmp_robot *robot, int64_t n_edges);
+int vmp_validate_motions_host(const vmp_robot *robot, const vmp_env *env, const float *starts_host,
+                              const float *goals_host, int64_t n_edges, int64_t sld,
+                              double resolution, int32_t width, uint32_t flags,
+                              uint32_t *bits_host, int32_t *n_states_host, int32_t *blocks_host,
+                              void *scratch, int64_t scratch_bytes, void *workspace,
+                              int64_t workspace_bytes, void *stream);
+
+/* FP32 FMA-pipe microbenchmark: `launches` back-to-back launches of a kernel
+ * of 8 independent FFMA chains per thread (4 x 256-thread CTAs per SM,
+ * 2 * 128 * iters flop per thread per launch), timed with CUDA events on a
+ * private stream; returns the achieved TFLOP/s (and ms).  bench.py uses it
+ * as the measured roofline denominator of this FP32-bound path (burst: one
+ * launch of a few ms; sustained: seconds of launches). */
+int vmp_bench_ffma(int64_t iters, int32_t launches, double *tflops, double *ms);
+
 /* The states the rake visits (reference motion.py:32-78 strata,
  * lanes.py:91-103 interpolate_lanes), written in the rake kernels' position
  * order with the same device arithmetic, for parity checks and callers that

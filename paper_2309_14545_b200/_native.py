@@ -46,7 +46,8 @@ EXPORTS = (
     "vmp_validate", "vmp_validate_motions", "vmp_discretize", "vmp_sphere_hits",
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
     "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace", "vmp_robot_home",
-    "vmp_motion_states",
+    "vmp_motion_states", "vmp_bench_ffma", "vmp_validate_host", "vmp_validate_host_scratch_bytes",
+    "vmp_validate_motions_host", "vmp_motions_host_scratch_bytes",
 )
 VMP_KNN_MAX_K = 32
 VMP_KNN_MAX_DIM = 64
@@ -114,6 +115,13 @@ def lib() -> ctypes.CDLL:
                                   vp, c_i64, vp], ctypes.c_int),
         "vmp_motion_workspace_bytes": ([c_i64], c_i64),
         "vmp_discretize": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, vp, vp], ctypes.c_int),
+        "vmp_validate_host": ([vp, vp, vp, c_i64, c_i64, c_u32, vp, vp, c_i64, vp], ctypes.c_int),
+        "vmp_validate_host_scratch_bytes": ([vp, c_i64], c_i64),
+        "vmp_validate_motions_host": ([vp, vp, vp, vp, c_i64, c_i64, c_dbl, c_i32, c_u32, vp, vp, vp,
+                                       vp, c_i64, vp, c_i64, vp], ctypes.c_int),
+        "vmp_motions_host_scratch_bytes": ([vp, c_i64], c_i64),
+        "vmp_bench_ffma": ([c_i64, c_i32, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)],
+                           ctypes.c_int),
         "vmp_motion_states": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, c_i32, c_u32, vp, vp, vp, vp],
                               ctypes.c_int),
         "vmp_sphere_hits": ([vp, vp, c_i64, c_i64, ctypes.c_float, vp, vp], ctypes.c_int),

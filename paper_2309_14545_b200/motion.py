@@ -71,15 +71,13 @@ def raked_motion_check(start: Config, goal: Config, ctx: ValidationContext,
     if s.shape[0] != ctx.program.dof:
         raise ValueError(f"block dim {s.shape[0]} != program dof {ctx.program.dof}")
     ctx.motion_checks += 1
-    sd = runtime.to_device(s.reshape(1, -1))
-    gd = runtime.to_device(g.reshape(1, -1))
-    bits, _, blocks = runtime.validate_motions_device(
-        *_bind(ctx), sd, gd, resolution, width=ctx.width, backward=backward,
-        prune=getattr(ctx, "prune", True), want_counts=True)
-    verdict = bool(int(bits[0].item()) & 1)
-    nblocks = int(blocks[0].item())
+    # one host-buffer C call: pinned staging -> plan + rake + finalize -> read-back
+    verdict, _, blocks = runtime.motions_host(*_bind(ctx), s.reshape(1, -1), g.reshape(1, -1),
+                                              resolution, width=ctx.width, backward=backward,
+                                              prune=getattr(ctx, "prune", True))
+    nblocks = int(blocks[0])
     ctx.blocks_evaluated += nblocks
-    return verdict, nblocks
+    return bool(verdict[0]), nblocks
 
 
 def validate_motion_rake(start: Config, goal: Config, ctx: ValidationContext,
