@@ -42,7 +42,7 @@ def timed(fn, reps=20, flush=None):
 
 def main():
     torch.cuda.set_device(0)
-    peak, _ = bench.fp32_peak_tflops()
+    peak = bench.nominal_fp32_tflops()
     hbm = 6539.9
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     rob = load_robot("arm7")
