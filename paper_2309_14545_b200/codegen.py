@@ -196,16 +196,24 @@ def _values_at_zero(program) -> np.ndarray:
     return val
 
 
+HOME_RADIUS = 2.0    # m: robots whose sphere centroid is nearer the origin keep the world frame
+
+
 def robot_home(program) -> tuple:
     """Origin of the environment frame the collision kernels work in: the mean
     sphere centre at the zero configuration, rounded to 1/64 m (exact in
-    float32).  Obstacle records are packed relative to it (vmp_env_create_at),
+    float32), or the world origin when that centroid lies within
+    ``HOME_RADIUS``.  Obstacle records are packed relative to it (vmp_env_create_at),
     so the expanded test forms (|c|^2 + |o|^2 - 2 c.o) never cancel
     |c|^2-sized terms for a robot far from the world origin."""
     if not program.checks:
         return (0.0, 0.0, 0.0)
     val = _values_at_zero(program)
     c = np.asarray([[val[v] for v in m.xyz] for m in program.checks]).mean(axis=0)
+    if np.linalg.norm(c) <= HOME_RADIUS:
+        # near the world origin the expanded forms are accurate to < 2e-5 m
+        # (DESIGN.md §4) and the unshifted sums are ~1 % faster in the rake
+        return (0.0, 0.0, 0.0)
     return tuple(float(v) for v in np.round(c * 64.0) / 64.0)
 
 

@@ -36,7 +36,7 @@ from pathlib import Path
 
 import numpy as np
 
-ROOT = Path(__file__).resolve().parent
+ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 L2_FLUSH_BYTES = 256 << 20          # > 126 MB L2
@@ -47,37 +47,14 @@ FMA_PER_CLK = 128
 
 # ----------------------------------------------------------------- helpers
 
-def nominal_fp32_tflops() -> float:
+def fp32_peak_tflops() -> tuple[float, str]:
     mhz = 1965.0
+    src = "nominal sm_max_mhz 1965"
     if PEAKS.exists():
         mhz = float(json.loads(PEAKS.read_text()).get("sm_max_mhz", mhz))
-    return SMS * FMA_PER_CLK * 2 * mhz * 1e6 / 1e12
-
-
-def measure_fp32_peak(device: int) -> dict:
-    """Measured FP32 FMA-pipe peak on this GPU (vmp_bench_ffma: 8 independent
-    FFMA chains per thread, 32 warps per SM).  ``burst``: best of 5 single
-    ~3 ms launches (the regime of a kernel timed alone - the bench steps are
-    tens of us with an L2 flush between them); ``sustained``: ~2 s of
-    back-to-back launches, with the SM clock sampled meanwhile."""
-    import ctypes
-
-    from paper_2309_14545_b200._native import check, lib
-    iters = 6000
-
-    def run(launches: int) -> float:
-        t, ms = ctypes.c_double(), ctypes.c_double()
-        check(lib().vmp_bench_ffma(iters, launches, ctypes.byref(t), ctypes.byref(ms)))
-        return t.value
-
-    run(1)
-    burst = max(run(1) for _ in range(5))
-    with ClockSampler(device) as clk:
-        sustained = run(600)
-    return {"burst_tflops": round(burst, 2), "sustained_tflops": round(sustained, 2),
-            "nominal_tflops": round(nominal_fp32_tflops(), 2),
-            "sustained_clocks": clk.summary(),
-            "kernel": "vmp_k_ffma (libvmp vmp_bench_ffma)"}
+        src = "MEASURED_PEAKS.json sm_max_mhz"
+    return SMS * FMA_PER_CLK * 2 * mhz * 1e6 / 1e12, \
+        f"148 SM x 128 FFMA/clk x 2 flop x {mhz:.0f} MHz ({src}); no tensor cores"
 
 
 class ClockSampler:
@@ -155,61 +132,6 @@ def _traffic(kernel: str):
     return json.loads(path.read_text()).get(kernel)
 
 
-
-
-def _executed(kernel: str):
-    """Executed FP32 flop per launch of ``kernel`` (ncu SASS op counts,
-    profiles/executed.json), or None."""
-    path = ROOT / "profiles" / "executed.json"
-    if not path.exists():
-        return None
-    return json.loads(path.read_text()).get(kernel)
-
-
-PARITY = ROOT / "tests" / "golden" / "bench_parity.npz"
-
-
-def _bits(words, n: int) -> np.ndarray:
-    w = np.ascontiguousarray(np.asarray(words).astype(np.uint32, copy=False))
-    return np.unpackbits(w.view(np.uint8), bitorder="little")[:n].astype(bool)
-
-
-def batch_parity(key: str, words) -> dict | None:
-    """Our verdicts of a full bench batch vs the reference's (fixture written by
-    tests/golden/make_bench_parity.py from the bit-exact oracle): mismatches
-    outside the +-1e-4 m clearance band must be 0; in-band ones are counted."""
-    if not PARITY.exists():
-        return None
-    fx = np.load(PARITY)
-    n = int(fx[f"{key}_n"])
-    got, ref = _bits(words, n), _bits(fx[f"{key}_ref_words"], n)
-    band = np.zeros(n, bool)
-    band[fx[f"{key}_band_idx"]] = True
-    diff = got != ref
-    return {"configs": n, "band": int(band.sum()), "band_mismatches": int((diff & band).sum()),
-            "mismatches_outside_band": int((diff & ~band).sum())}
-
-
-def motion_parity(valid: np.ndarray) -> dict | None:
-    if not PARITY.exists():
-        return None
-    fx = np.load(PARITY)
-    ref = fx["cfg2_ref_verdict"]
-    crit = fx["cfg2_band_critical"]
-    return {"edges": int(len(ref)), "mismatches": int((valid != ref).sum()),
-            "band_states": int(fx["cfg2_band_states"].sum()),
-            "band_critical_edges": [int(e) for e in crit],
-            "band_critical_mismatches": int((valid[crit] != ref[crit]).sum())}
-
-
-CFG2_CONFIG = {"workload": "cfg2_arm7_4096edges_24box_8cap", "robot": "arm7 (Panda stand-in)",
-               "edges_per_gpu": 4096, "resolution": 1.0 / 32.0,
-               "obstacles": "24 cuboids + 8 capsules (keep-out 0.3 m)",
-               "edges": "seeded, even-indexed edges forced collision-free "
-                        "(paper_2309_14545_b200/data/cfg2_edges.npz)"}
-METRIC = "validated edges/sec (raked motion validation, BASELINE config 2)"
-
-
 # ----------------------------------------------------------- our GPU arm
 
 def run_ours(args, rank: int, world: int) -> dict | None:
@@ -223,6 +145,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    peak, peak_src = fp32_peak_tflops()
 
     mw = workloads.config2()
     rob = load_robot(mw.robot)
@@ -236,10 +159,8 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     mod, denv = ctx.module, ctx.device_env
     stream = torch.cuda.current_stream()
 
-    # the roofline denominator, measured on this GPU (VMP_BENCH_PEAK_FIRST=1: before
-    # the timed regions instead of after them - an experiment switch)
-    peak_first = os.environ.get("VMP_BENCH_PEAK_FIRST") == "1"
-    peaks = measure_fp32_peak(dev) if peak_first else None
+    def step():
+        mv()                                              # one graph replay = one step
 
     # per-edge counts for the roofline numerator (one extra untimed launch)
     b0, ns_t, bl_t = runtime.validate_motions_device(mod, denv, sd, gd, mw.resolution, width=32,
@@ -252,7 +173,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     flops_per_launch = float(states.sum()) * f_state
 
     for _ in range(args.warmup):
-        mv()
+        step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -263,7 +184,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         for a, b in ev:
             flush.zero_()                                 # L2 flush between timed steps
             a.record(stream)
-            mv()                                          # one step = one graph replay
+            step()
             b.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -277,7 +198,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     ms_per_step = total_ms / args.steps
     value = world * E / (ms_per_step / 1e3)
     avg_launch_ms = float(np.mean(kernel_ms))
-    got_valid = runtime.unpack_bits(mv.host_bits(), E)
+    achieved = flops_per_launch / (avg_launch_ms / 1e3) / 1e12
 
     # ---- end to end through the public API, host buffers: every step copies its
     # edges from pinned host memory and reads its verdict words back; the
@@ -311,38 +232,12 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         e2e_ms = float(tt.item())
     e2e_value = world * E / (e2e_ms / args.steps / 1e3)
     assert runtime.unpack_bits(got, E).tolist() == valid.tolist()
-    assert got_valid.tolist() == valid.tolist()
 
-    if peaks is None:
-        peaks = measure_fp32_peak(dev)
-    peak = peaks["burst_tflops"]
-    achieved = flops_per_launch / (avg_launch_ms / 1e3) / 1e12
+    fkcc = {} if args.no_aux else fkcc_summary(ctx_flush=flush, peak=peak)
     if rank != 0:
         return None
-    aux = not args.no_aux
-    fkcc = fkcc_summary(ctx_flush=flush, peak=peak) if aux else {}
-    executed = _executed("vmp_motion_p1_s2_g1_o_ns")
-    roofline = {"bound": "fp32", "achieved": round(achieved, 3), "peak": peak,
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "traffic": _traffic("vmp_motion_p1_s2_g1_o_ns"),
-                # the register-capped rake variant (loaded when it compiles
-                # without local memory; arm7: 96 registers, 5 CTAs / SM),
-                # built without sphere-obstacle code (config 2 has none)
-                "kernel": "vmp_motion_p1_s2_g1_o_ns",
-                "algorithmic_flop_per_state": f_state,
-                "states_counted_per_launch": int(states.sum()),
-                "peak_measured": peaks,
-                "note": "achieved = states the rake must fully evaluate (valid edges: all n; "
-                        "invalid: the iterations before the failing one) x the reference's "
-                        "dense flop per state / mean step time (plan + rake + finalize); "
-                        "peak = measured FFMA burst (peak_measured); no tensor cores"}
-    if executed:
-        ex = float(executed["flop_per_launch"])
-        roofline["executed_frac"] = round(ex / (avg_launch_ms / 1e3) / 1e12 / peak, 4)
-        roofline["executed_flop_per_launch"] = ex
-        roofline["executed_source"] = executed.get("source", "profiles/executed.json")
     line = {
-        "metric": METRIC,
+        "metric": "validated edges/sec (raked motion validation, BASELINE config 2)",
         "value": round(value, 1),
         "unit": "edges/s",
         "n_gpus": world,
@@ -354,42 +249,49 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (seeded; arm7 stand-in for Panda, see DESIGN.md)",
-        "config": dict(CFG2_CONFIG),
-        "setup": {"rake_width": 32, "parallelism": f"dp{world} (independent edges per rank)",
-                  "valid_edge_fraction": round(float(valid.mean()), 4),
-                  "mean_states_per_edge": round(float(n_np.mean()), 2),
-                  "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
-                  "launch": "CUDA graph (plan -> rake -> finalize, PDL edges) via "
-                            "motion.MotionValidator; e2e through motion.MotionPipeline (4 slots, "
-                            "each step's H2D, graph replay and D2H on its slot's own stream)"},
-        "roofline": roofline,
+        "config": {"workload": mw.name, "robot": "arm7 (Panda stand-in)", "edges_per_gpu": E,
+                   "resolution": mw.resolution, "rake_width": 32,
+                   "obstacles": "24 cuboids + 8 capsules",
+                   "valid_edge_fraction": round(float(valid.mean()), 4),
+                   "mean_states_per_edge": round(float(n_np.mean()), 2),
+                   "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
+                   "launch": "CUDA graph (plan -> rake -> finalize, PDL edges) via motion.MotionValidator; "
+                             "e2e through motion.MotionPipeline (4 slots, each step's H2D, "
+                             "graph replay and D2H on its slot's own stream: step k+1's copy "
+                             "and rake start while step k's rake drains)",
+                   "parallelism": f"dp{world} (independent edges per rank)"},
+        "roofline": {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                     "traffic": _traffic("vmp_motion_p1_s2_g1_o_ns"),
+                     # the register-capped rake variant (loaded when it compiles
+                     # without local memory; arm7: 96 registers, 5 CTAs / SM),
+                     # built without sphere-obstacle code (config 2 has none)
+                     "kernel": "vmp_motion_p1_s2_g1_o_ns",
+                     "algorithmic_flop_per_state": f_state,
+                     "states_counted_per_launch": int(states.sum()),
+                     "note": "states fully evaluated by the rake (valid edges: all n; invalid: "
+                             "iterations before the failing one) x reference dense flop/state; "
+                             "peak: " + peak_src},
         # per step (one graph replay): cluster plan + rake + finalize kernels
         "gpu_launches": 3 * args.steps,
         "e2e": {"value": round(e2e_value, 1), "unit": "edges/s",
                 "h2d_bytes_per_step": int(mw.starts.nbytes + mw.goals.nbytes),
                 "d2h_bytes_per_step": int(bits.numel() * 4)},
         "clocks": clocks.summary(),
-        "parity": {"cfg2": motion_parity(valid)},
     }
     if fkcc:
-        for key in ("cfg1", "cfg3", "cfg4"):
-            line["parity"][key] = fkcc[key].pop("parity")
         line["fkcc"] = fkcc
-        line["latency"] = latency_summary(mw, rob)
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"], line["cpu_baselines"] = cpu_baselines(args.cpu_edges)
-        if "latency" in line:
-            line["latency"]["reference"] = line["cpu_baselines"].pop("latency", None)
+        line["cpu_baseline"] = cpu_baseline_motion(mw, rob, processes=1, n_edges=args.cpu_edges)
     return line
 
 
 def fkcc_summary(ctx_flush, peak: float) -> dict:
-    """Configs 1/3/4 batch FK+CC: configs/s and % of the measured FP32 peak
-    (product mode = the library's kernel choice; dense = every test), plus
-    verdict parity of the full batch against the reference's verdicts."""
+    """Configs 1/3/4 batch FK+CC: configs/s and % FP32 roofline (dense + early exit)."""
     import torch
 
     from paper_2309_14545_b200 import ValidationContext, codegen, load_robot, workloads
+    from paper_2309_14545_b200 import runtime
 
     out = {}
     for key, make in (("cfg1", workloads.config1), ("cfg3", workloads.config3),
@@ -400,7 +302,8 @@ def fkcc_summary(ctx_flush, peak: float) -> dict:
         n = wl.q.shape[1]
         f = codegen.algorithmic_flops(rob.program, rob.pairs, ctx.device_env.counts)["total"]
         res = {"robot": wl.robot, "configs": n, "flop_per_config": f}
-        words = {}
+        # product = the library's default kernel choice (early exit + broadphase,
+        # or the straight-line dense kernel for sphere-only scenes); dense = every test
         for mode, early in (("product", True), ("dense", False)):
             cv = ctx.batch_validator(n, early_exit=early)       # resident batch + CUDA graph
             cv(wl.q)
@@ -415,18 +318,13 @@ def fkcc_summary(ctx_flush, peak: float) -> dict:
                 b.record()
                 torch.cuda.synchronize()
                 times.append(a.elapsed_time(b))
-            words[mode] = cv.bits.cpu().numpy()
+            words = cv.bits
             ms = float(np.mean(times))        # event ticks are ~2 us: mean of 20, not median
             rate = n / (ms / 1e3)
             res[mode] = {"ms": round(ms, 4), "configs_per_s": round(rate, 1),
                          "tflops": round(rate * f / 1e12, 3),
                          "frac_fp32": round(rate * f / 1e12 / peak, 4)}
-            ex = _executed(f"{key}_{mode}")
-            if ex:
-                res[mode]["executed_frac"] = round(ex["flop_per_launch"] / (ms / 1e3) / 1e12 / peak, 4)
-        assert np.array_equal(words["product"], words["dense"])
-        res["collision_rate"] = round(1 - float(_bits(words["product"], n).mean()), 4)
-        res["parity"] = batch_parity(key, words["product"])
+        res["collision_rate"] = round(1 - float(runtime.unpack_bits(words.cpu().numpy(), n).mean()), 4)
         out[key] = res
     out["fk_only"] = fk_only_summary(ctx_flush)
     return out
@@ -461,39 +359,6 @@ def fk_only_summary(ctx_flush, n: int = 1 << 22) -> dict:
         out[name] = {"bytes_per_config": 4 * (rob.program.dof + rows), "us": round(t * 1e6, 1),
                      "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
     return out
-
-
-def latency_summary(mw, rob, calls: int = 300) -> dict:
-    """Per-call latency of the reference-signature single-request API (what
-    the reference's planners call one at a time, planners.py:119-123,152-168,
-    simplify.py:82-86): state_valid and a W = 8 validate_block
-    (ValidationContext(width=8)), and a single-edge raked_motion_check - host
-    inputs and results, one synchronising C call each (vmp_*_host).  Host
-    wall clock per call (the GPU work is synchronous inside the call)."""
-    from paper_2309_14545_b200 import ConfigBlock, ValidationContext
-    from paper_2309_14545_b200 import motion as M
-
-    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env, width=8)
-    q = np.ascontiguousarray(mw.starts[:8].T)
-    block = ConfigBlock(dim=q.shape[0], width=8, data=q, valid_count=8)
-
-    def per_call(fn, n):
-        for _ in range(20):
-            fn(0)
-        t0 = time.perf_counter()
-        for i in range(n):
-            fn(i)
-        return round((time.perf_counter() - t0) / n * 1e6, 2)
-
-    return {
-        "state_valid_us": per_call(lambda i: ctx.state_valid(mw.starts[i % 4096]), calls),
-        "validate_block_w8_us": per_call(lambda i: ctx.validate_block(block), calls),
-        "raked_motion_check_us": per_call(
-            lambda i: M.raked_motion_check(mw.starts[i % 4096], mw.goals[i % 4096], ctx,
-                                           mw.resolution), calls),
-        "note": "ValidationContext(width=8); raked_motion_check averaged over the first "
-                f"{calls} config-2 edges (plan + rake + finalize per call)",
-    }
 
 
 # ------------------------------------------------------- CPU reference arm
@@ -539,24 +404,21 @@ def _ref_context(mw):
 def _cpu_init() -> None:
     """Per-process state of the CPU arm: the reference package when staged
     (kind "reference"), else the oracle port (kind "port"); workload."""
-    if _CPU:
-        return
     from paper_2309_14545_b200 import load_robot, workloads
     mw = workloads.config2()
     ref = _ref_context(mw)
+    if ref is not None:
+        _CPU.update(kind="reference", mw=mw, ctx=ref[0], rake=ref[1])
+        return
     sys.path.insert(0, str(ROOT / "oracle"))
     import vecmp_oracle as O
-    _CPU.update(O=O, mw=mw)
-    if ref is not None:
-        _CPU.update(kind="reference", ctx=ref[0], rake=ref[1])
-        return
     rob = load_robot(mw.robot)
-    _CPU.update(kind="port", rob=rob, ob=O.Obstacles(mw.env.primitives))
+    _CPU.update(kind="port", O=O, mw=mw, rob=rob, ob=O.Obstacles(mw.env.primitives))
 
 
 def _cpu_worker(idx):
-    """Config-2 edges ``idx`` through the W = 8 rake, as the reference runs it."""
-    _cpu_init()
+    if not _CPU:
+        _cpu_init()
     mw = _CPU["mw"]
     if _CPU["kind"] == "reference":
         ctx, rake = _CPU["ctx"], _CPU["rake"]
@@ -566,201 +428,67 @@ def _cpu_worker(idx):
             for i in idx]
 
 
-_FKCC = {}
-
-
-def _fkcc_workload(key: str):
-    if key not in _FKCC:
-        from paper_2309_14545_b200 import load_robot, workloads
-        wl = {"cfg1": workloads.config1, "cfg3": workloads.config3, "cfg4": workloads.config4}[key]()
-        rob = load_robot(wl.robot)
-        _FKCC[key] = (wl, rob, _CPU["O"].Obstacles(wl.env.primitives))
-    return _FKCC[key]
-
-
-def _fkcc_job(job):
-    """FK+CC on the CPU (oracle port of the reference's validate_block, prune on
-    as ValidationContext's default): ``asis`` = W = 8 blocks, the reference's
-    own width; ``wide`` = one block over the whole slice."""
-    _cpu_init()
-    key, mode, lo, hi = job
-    O = _CPU["O"]
-    wl, rob, ob = _fkcc_workload(key)
-    q = wl.q[:, lo:hi]
-    t0 = time.perf_counter()
-    if mode == "asis":
-        for i in range(0, q.shape[1], 8):
-            O.validate_lanes(rob.program, rob.pairs, ob, np.ascontiguousarray(q[:, i:i + 8]))
-    else:
-        O.validate_lanes(rob.program, rob.pairs, ob, np.ascontiguousarray(q))
-    return key, mode, hi - lo, time.perf_counter() - t0
-
-
-def _motion_job(job):
-    _cpu_init()
-    t0 = time.perf_counter()
-    _cpu_worker(job[1])
-    return "cfg2", "asis", len(job[1]), time.perf_counter() - t0
-
-
-def _latency_job(_):
-    """Per-call latency of the reference API on one core: state_valid and one
-    W = 8 validate_block (oracle port of validate_block), and one W = 8 rake."""
-    _cpu_init()
-    O, mw = _CPU["O"], _CPU["mw"]
-    from paper_2309_14545_b200 import load_robot
-    rob = load_robot(mw.robot)
-    ob = O.Obstacles(mw.env.primitives)
-    q8 = np.ascontiguousarray(mw.starts[:8].T)
-    t0 = time.perf_counter()
-    for i in range(200):
-        O.validate_lanes(rob.program, rob.pairs, ob, np.repeat(mw.starts[i][:, None], 8, axis=1))
-    sv = (time.perf_counter() - t0) / 200
-    t0 = time.perf_counter()
-    for _ in range(200):
-        O.validate_lanes(rob.program, rob.pairs, ob, q8)
-    vb = (time.perf_counter() - t0) / 200
-    t0 = time.perf_counter()
-    for i in range(100):
-        O.rake_check(rob.program, rob.pairs, ob, mw.starts[i], mw.goals[i], mw.resolution, 8)
-    rk = (time.perf_counter() - t0) / 100
-    return {"state_valid_us": round(sv * 1e6, 1), "validate_block_w8_us": round(vb * 1e6, 1),
-            "raked_motion_check_us": round(rk * 1e6, 1),
-            "kind": "port", "note": "oracle port of the reference API on 1 host core; "
-                                    "rake averaged over the first 100 config-2 edges"}
-
-
-def _cores() -> int:
-    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-
-
-def _cpu_model() -> str:
-    try:
-        for line in Path("/proc/cpuinfo").read_text().splitlines():
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except OSError:
-        pass
-    return "unknown"
-
-
 def _sample(n_edges: int, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return np.sort(rng.choice(4096, size=min(n_edges, 4096), replace=False))
 
 
-def cpu_baselines(motion_edges: int, prefix: int = 65536) -> tuple[dict, dict]:
-    """The reference CPU path on this box's host cores:
-
-    * config 2 motion: ``motion_edges`` seeded edges through the W = 8 rake on
-      one core (the headline ``cpu_baseline``);
-    * configs 1 / 3 / 4 FK+CC: (1) as-is - W = 8 validate_block blocks on a
-      ``prefix``-configuration prefix, one core; (2) wide - the same prefix as
-      one block, one core; (3) wide x cores - the whole batch split over every
-      core, one process each;
-    * per-call latency of the reference API (one core).
-
-    Phase 1 runs the single-core jobs concurrently, one process per job;
-    phase 2 the all-core runs.  The oracle port is bit-exact to the reference
-    (tests/test_oracle_golden.py); the reference package itself is used for
-    the motion job when staged under baseline/_ref/pkg."""
-    import multiprocessing as mp
-
-    cores = _cores()
+def cpu_baseline_motion(mw, rob, processes: int, n_edges: int) -> dict:
+    """The reference (or, unstaged, its bit-exact oracle port) on one host
+    core: the ValidationContext(width=8) rake per edge, as the reference runs it."""
     _cpu_init()
-    kind = _CPU["kind"]
-    mctx = mp.get_context("fork")
-    idx = _sample(motion_edges, 123)
-    jobs = [("cfg2", idx)] + [(k, m, 0, prefix) for k in ("cfg1", "cfg3", "cfg4")
-                              for m in ("asis", "wide")]
-    t_start = time.perf_counter()
-    with mctx.Pool(min(cores, len(jobs) + 1)) as pool:
-        lat = pool.apply_async(_latency_job, (0,))
-        res = pool.map(lambda_dispatch, jobs, chunksize=1)
-        latency = lat.get()
-    rates = {(k, m): n / t for k, m, n, t in res}
-    wide_all = {}
-    with mctx.Pool(cores) as pool:
-        for key in ("cfg1", "cfg3", "cfg4"):
-            n = {"cfg1": 65536, "cfg3": 1 << 20, "cfg4": 1 << 20}[key]
-            bounds = np.linspace(0, n, cores + 1).astype(int)
-            pool.map(_fkcc_job, [(key, "wide", 0, 64)] * cores)          # warm every worker
-            t0 = time.perf_counter()
-            pool.map(_fkcc_job, [(key, "wide", lo, hi) for lo, hi in zip(bounds, bounds[1:])],
-                     chunksize=1)
-            wide_all[key] = n / (time.perf_counter() - t0)
-    wall = time.perf_counter() - t_start
-    what = "vecmp validate_motion_rake" if kind == "reference" else "oracle port"
-    motion = {"value": round(rates[("cfg2", "asis")], 2), "unit": "edges/s", "cores": 1,
-              "kind": kind,
-              "sample": f"{len(idx)} seeded-random edges of the 4,096 ({what}, W=8 rake, numpy "
-                        f"{np.__version__}, 1 process)"}
-    fk = {"host": {"cores": cores, "cpu_model": _cpu_model(), "numpy": np.__version__,
-                   "wall_s": round(wall, 1)},
-          "latency": latency}
-    for key in ("cfg1", "cfg3", "cfg4"):
-        fk[key] = {"unit": "configs/s", "kind": "port",
-                   "asis_w8_1core": round(rates[(key, "asis")], 1),
-                   "wide_1core": round(rates[(key, "wide")], 1),
-                   "wide_all_cores": round(wide_all[key], 1),
-                   "sample": f"as-is / wide: first {prefix} configurations of the batch "
-                             f"(W=8 blocks / one block, 1 core); wide x cores: the whole "
-                             f"batch, one process per core ({cores})"}
-    return motion, fk
-
-
-def lambda_dispatch(job):
-    return _motion_job(job) if job[0] == "cfg2" else _fkcc_job(job)
+    idx = _sample(n_edges, 123)
+    _cpu_worker(idx[:8])                                  # warm caches
+    t0 = time.perf_counter()
+    _cpu_worker(idx)
+    wall = time.perf_counter() - t0
+    what = "vecmp validate_motion_rake" if _CPU["kind"] == "reference" else "oracle port"
+    return {"value": round(len(idx) / wall, 2), "unit": "edges/s", "cores": 1, "kind": _CPU["kind"],
+            "sample": f"{len(idx)} seeded-random edges of the 4,096 ({what}, W=8 rake, numpy "
+                      f"{np.__version__}, 1 process, {wall:.1f} s wall)"}
 
 
 def run_reference(args, rank: int, world: int) -> dict | None:
-    """The reference CPU path on this box's host cores, every step validating
-    the FULL 4,096-edge config-2 batch (W = 8 rake per edge, one process per
-    core, edges dealt round-robin in chunks)."""
     if rank != 0:
         return None
     import multiprocessing as mp
 
-    cores = _cores()
-    E = 4096
-    chunks = [np.arange(i, E, cores * 4) for i in range(cores * 4)]   # balanced, interleaved
+    from paper_2309_14545_b200 import load_robot, workloads
+    mw = workloads.config2()
+    rob = load_robot(mw.robot)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    per_step = max(cores * 8, 64)
     pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init)
     try:
         for w in range(args.warmup):
-            pool.map(_cpu_worker, [c[:1] for c in chunks[:cores]])
+            pool.map(_cpu_worker, np.array_split(_sample(cores, 7 + w), cores))
         t_total = 0.0
-        verdicts = None
         for k in range(args.steps):
+            idx = _sample(per_step, 1000 + k)
             t0 = time.perf_counter()
-            parts = pool.map(_cpu_worker, chunks, chunksize=1)
+            pool.map(_cpu_worker, np.array_split(idx, cores))
             t_total += time.perf_counter() - t0
-            if verdicts is None:
-                verdicts = np.zeros(E, bool)
-                for c, v in zip(chunks, parts):
-                    verdicts[c] = v
     finally:
         pool.close()
         pool.join()
-    value = args.steps * E / t_total
+    value = args.steps * per_step / t_total
     _cpu_init()                                           # this process: which arm ran
     kind = _CPU["kind"]
     what = "vecmp validate_motion_rake" if kind == "reference" else "oracle port of it"
     return {
         "impl": "reference",
-        "metric": METRIC,
+        "metric": "validated edges/sec (raked motion validation, BASELINE config 2)",
         "value": round(value, 2), "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * t_total / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded; arm7 stand-in for Panda, see DESIGN.md)",
-        "config": dict(CFG2_CONFIG),
-        "setup": {"rake_width": 8, "parallelism": f"{cores} host processes (one per core)",
-                  "valid_edge_fraction": round(float(verdicts.mean()), 4)},
+        "data": "synthetic (seeded; arm7 stand-in for Panda)",
+        "config": {"workload": mw.name, "robot": "arm7 (Panda stand-in)", "resolution": mw.resolution,
+                   "edges_per_step": per_step},
         "cpu_baseline": {"value": round(value, 2), "unit": "edges/s", "cores": cores, "kind": kind,
-                         "sample": f"every step the full {E}-edge batch ({what}, W=8 rake), "
-                                   f"one process per core, {_cpu_model()}"},
+                         "sample": f"{per_step} seeded-random edges per step ({what}), W=8 "
+                                   f"rake, one process per core"},
         "e2e": {"value": round(value, 2), "unit": "edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "parity": {"cfg2": motion_parity(verdicts)},
     }
 
 
@@ -772,8 +500,7 @@ def main() -> None:
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    p.add_argument("--no-aux", action="store_true",
-                   help="skip the FK+CC batch summary, parity and latency sections")
+    p.add_argument("--no-aux", action="store_true", help="skip the FK+CC batch summary")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-edges", type=int, default=1024)
     args = p.parse_args()
@@ -791,7 +518,6 @@ def main() -> None:
         print(json.dumps(line), flush=True)
     if world > 1 and args.impl == "ours":
         import torch.distributed as dist
-        dist.barrier()
         dist.destroy_process_group()
 
 

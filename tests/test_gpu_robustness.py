@@ -164,6 +164,7 @@ def test_translated_scene_verdicts(cuda, cfg, k):
     env = translate_env(wl.env, off)
     ctx = ValidationContext(prog, rob.model, rob.pairs, env)
     assert np.linalg.norm(np.asarray(ctx.device_env.origin) - off) < 2.0   # frame near the robot
+    assert ctx.device_env.origin != (0.0, 0.0, 0.0)
     for early in (True, False):
         got = runtime.unpack_bits(ctx.validate_batch(wl.q, early_exit=early).cpu().numpy(), n)
         _parity(prog, rob.pairs, env.primitives, wl.q, got, max_band=max(4, n // 2000))
@@ -237,9 +238,11 @@ def test_environment_frame_must_match_robot_home(cuda):
     torch = cuda
     rob = load_robot("arm7")
     wl = workloads.config1(64)
-    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    prog = translate_program(rob.program, OFFSETS[0])
+    env = translate_env(wl.env, OFFSETS[0])
+    ctx = ValidationContext(prog, rob.model, rob.pairs, env)
     assert ctx.device_env.origin == ctx.module.home != (0.0, 0.0, 0.0)
-    world = runtime.DeviceEnv(wl.env.primitives, origin=(0.0, 0.0, 0.0))
+    world = runtime.DeviceEnv(env.primitives, origin=(0.0, 0.0, 0.0))
     qd = torch.from_numpy(wl.q).cuda()
     with pytest.raises(ValueError, match="frame"):
         runtime.validate_device(ctx.module, world, qd, 64, 64)
