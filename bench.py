@@ -55,15 +55,15 @@ def nominal_fp32_tflops() -> float:
 
 
 def measure_fp32_peak(device: int) -> dict:
-    """Measured FP32 FMA-pipe peak on this GPU (vmp_bench_ffma: 8 independent
-    FFMA chains per thread, 32 warps per SM).  ``burst``: best of 5 single
+    """Measured FP32 FMA-pipe peak on this GPU (vmp_bench_ffma: 4 independent
+    FFMA chains per thread, 64 warps per SM).  ``burst``: best of 5 single
     ~3 ms launches (the regime of a kernel timed alone - the bench steps are
     tens of us with an L2 flush between them); ``sustained``: ~2 s of
     back-to-back launches, with the SM clock sampled meanwhile."""
     import ctypes
 
     from paper_2309_14545_b200._native import check, lib
-    iters = 6000
+    iters = 1500
 
     def run(launches: int) -> float:
         t, ms = ctypes.c_double(), ctypes.c_double()

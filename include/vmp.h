@@ -164,8 +164,8 @@ int vmp_validate_motions_host(const vmp_robot *robot, const vmp_env *env, const 
                               int64_t workspace_bytes, void *stream);
 
 /* FP32 FMA-pipe microbenchmark: `launches` back-to-back launches of a kernel
- * of 8 independent FFMA chains per thread (4 x 256-thread CTAs per SM,
- * 2 * 128 * iters flop per thread per launch), timed with CUDA events on a
+ * of 4 independent FFMA chains per thread (8 x 256-thread CTAs per SM,
+ * 2 * 256 * iters flop per thread per launch), timed with CUDA events on a
  * private stream; returns the achieved TFLOP/s (and ms).  bench.py uses it
  * as the measured roofline denominator of this FP32-bound path (burst: one
  * launch of a few ms; sustained: seconds of launches). */
