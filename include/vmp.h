@@ -38,6 +38,10 @@ extern "C" {
 #define VMP_NO_SPLIT 8u      /* never use the small-batch split kernel               */
 #define VMP_FORCE_SPLIT 32u  /* always use it (tests)                                */
 #define VMP_TWO_PASS 64u     /* two-pass broadphase (bound mask per 32 obstacles)     */
+#define VMP_PDL 1024u        /* programmatic dependent launch: this batch may start
+                                while the previous kernel on the stream drains - only
+                                for inputs that kernel does not write (consecutive
+                                batches of resident configurations, ConfigStream)  */
 /* vmp_validate_motions flags (reference motion.py:38-90) */
 #define VMP_BACKWARD 16u     /* comb each stratum top-down (backward=True)            */
 #define VMP_OVERLAPPED 512u  /* batches overlap on several streams (a pipeline):

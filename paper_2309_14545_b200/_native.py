@@ -31,6 +31,7 @@ VMP_FORCE_SPLIT = 32
 VMP_TWO_PASS = 64
 VMP_BACKWARD = 16
 VMP_OVERLAPPED = 512
+VMP_PDL = 1024
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -40,6 +40,7 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
 SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
+SPLITS = (2, 4)         # split validate kernels emitted (x2: mid-size batches)
 MOTION_MIN_CTAS = 5     # occupancy target of the register-capped rake variant (6-8: spills, measured slower)
 FK_SMEM_TILE = 160 * 1024   # largest vmp_fk_spheres centre tile (shared memory bytes)
 
@@ -665,6 +666,9 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
   __shared__ unsigned vmp_part[{BLOCK} / 32];
+  // a following batch launched with VMP_PDL may start as soon as this grid's
+  // CTAs are resident (its inputs are its own; nothing here is waited for)
+  asm volatile("griddepcontrol.launch_dependents;");
   // the environment copy overlaps the joint loads, FK and self pairs of the
   // first tile; vmp_state waits for it before the first obstacle
   const float4 *env = STAGED ? vmp_smem : a.env.rec;
@@ -863,9 +867,10 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
                         f'vmp_validate_p{prune}_s{stop}_g{staged}(VmpValidateArgs a) '
                         f'{{ vmp_validate_body<{prune}, {stop}, {g}, 1>(a); }}\n')
                 if staged:
-                    src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
-                            f'vmp_validate_p{prune}_s{stop}_g1_x{SPLIT}(VmpValidateArgs a) '
-                            f'{{ vmp_validate_body<{prune}, {stop}, true, {SPLIT}>(a); }}\n')
+                    for sp in SPLITS:
+                        src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
+                                f'vmp_validate_p{prune}_s{stop}_g1_x{sp}(VmpValidateArgs a) '
+                                f'{{ vmp_validate_body<{prune}, {stop}, true, {sp}>(a); }}\n')
                 if staged and stop == 1:            # two-pass broadphase, small batches
                     for sp in (1, SPLIT):
                         src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '

@@ -14,9 +14,13 @@ from paper_2309_14545_b200 import ValidationContext, load_robot, runtime, worklo
 
 torch.cuda.set_device(0)
 flush = torch.empty(256 << 18, dtype=torch.float32, device="cuda")
+import os  # noqa: E402
 VARIANTS = {"x1": dict(split=False), "x1t": dict(split=False, two_pass=True),
             "x4": dict(split=True), "x4t": dict(split=True, two_pass=True),
             "dense": dict(split=False, early_exit=False), "dense4": dict(split=True, early_exit=False)}
+if os.environ.get("VMP_EXP_SPLIT"):   # the forced split count applies to every variant
+    VARIANTS = {"prod": dict(), "dense": dict(early_exit=False),
+                "prod_np": dict(prune=False), "dense_np": dict(early_exit=False, prune=False)}
 
 
 def timed(fn, reps=15):
@@ -34,8 +38,9 @@ def timed(fn, reps=15):
 
 
 cases = [("cfg1", workloads.config1(1048576), n) for n in (4096, 16384, 65536, 131072, 262144)]
-cases += [("cfg3", workloads.config3(), n) for n in (4096, 16384, 65536, 262144)]
-cases += [("cfg4", workloads.config4(), n) for n in (4096, 16384, 65536, 262144)]
+if not os.environ.get("VMP_EXP_CFG1_ONLY"):
+    cases += [("cfg3", workloads.config3(), n) for n in (4096, 16384, 65536, 262144)]
+    cases += [("cfg4", workloads.config4(), n) for n in (4096, 16384, 65536, 262144)]
 for name, wl, n in cases:
     rob = load_robot(wl.robot)
     ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)

@@ -112,3 +112,20 @@ def test_every_kernel_variant_gives_the_same_words(cuda, cfg):
                dict(split=True, early_exit=False)):
         got = runtime.validate_device(ctx.module, ctx.device_env, q, n, q.stride(0), **kw)
         assert np.array_equal(got.cpu().numpy(), ref), kw
+
+
+@pytest.mark.parametrize("cfg,n", [("cfg1", 65536), ("cfg3", 20000), ("cfg1", 1000)])
+def test_config_stream_pdl_chain(cuda, cfg, n):
+    """One graph of PDL-chained launches over distinct resident batches gives
+    every batch the verdicts of its own standalone launch."""
+    wl = workloads.config1(n) if cfg == "cfg1" else workloads.config3(n)
+    rob = load_robot(wl.robot)
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, wl.env)
+    batches = [workloads.uniform_configs(rob.limits, n, 900 + i) for i in range(7)]
+    cs = ctx.stream_validator(n, len(batches))
+    for i, q in enumerate(batches):
+        cs.load(i, q)
+    for _ in range(3):
+        out = cs()
+        for q, words in zip(batches, out):
+            assert np.array_equal(words.cpu().numpy(), ctx.validate_batch(q).cpu().numpy())
