@@ -40,7 +40,8 @@ CSRC = Path(__file__).resolve().parent / "csrc"
 BLOCK = 128
 GROUP_SIZE = 3          # dynamic spheres per broadphase group
 SPLIT = 4               # warps per configuration slice in the small-batch validate kernels
-SPLITS = (2, 4)         # split validate kernels emitted (x2: mid-size batches)
+SPLITS = (4,)           # split validate kernels emitted (a 2-warp split measured no
+                        # faster at 16K-256K configurations, scripts/exp_stream.py)
 MOTION_MIN_CTAS = 5     # occupancy target of the register-capped rake variant (6-8: spills, measured slower)
 FK_SMEM_TILE = 160 * 1024   # largest vmp_fk_spheres centre tile (shared memory bytes)
 
