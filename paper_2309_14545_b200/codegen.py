@@ -60,7 +60,9 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 28
+CODEGEN_VERSION = 30
+# packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
+FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
 # this before codegen runs); off in production - they cost ~2 % of the step
 TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
@@ -338,6 +340,26 @@ def _state_function(lay: RobotLayout, program) -> str:
         ex, ey, ez = _exyz(mid)
         emit(f"  const float G{gi}S = vmp_sphere_S({ex}, {ey}, {ez}, G{gi}R * G{gi}R);")
         emit(f"  const float G{gi}M = -2.0f * G{gi}R;")
+    # broadphase bound tests of two groups per packed FFMA2 chain (bit-identical
+    # to the scalar chains); an odd last group stays scalar
+    pairs = [(groups[i], i) for i in range(0, len(groups) - 1, 2)] if FFMA2 else []
+    for _, gi in pairs:
+        a, b = groups[gi], groups[gi + 1]
+        (ax, ay, az), (bx, by, bz) = _exyz(a[len(a) // 2]), _exyz(b[len(b) // 2])
+        emit(f"  const vmp_f2 Q{gi}X = vmp_pk({ax}, {bx}), Q{gi}Y = vmp_pk({ay}, {by}), "
+             f"Q{gi}Z = vmp_pk({az}, {bz});")
+        emit(f"  const vmp_f2 Q{gi}S = vmp_pk(G{gi}S, G{gi + 1}S), Q{gi}M = vmp_pk(G{gi}M, G{gi + 1}M);")
+
+    def bound_terms() -> list[str]:
+        """Per obstacle: the expanded bound distance of every group, as terms
+        whose minimum decides "near" (packed pairs first)."""
+        terms = [f"vmp_sphere_w2(Q{gi}X, Q{gi}Y, Q{gi}Z, Q{gi}S, Q{gi}M, bnd, brad)" for _, gi in pairs]
+        paired = {gi for _, gi in pairs} | {gi + 1 for _, gi in pairs}
+        for gi, grp in enumerate(groups):
+            if gi not in paired:
+                mx, my, mz = _exyz(grp[len(grp) // 2])
+                terms.append(f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)")
+        return terms
     # self-collision pairs (compile-time thresholds), bucketed by group pair;
     # constant spheres are singleton groups with their exact centre and radius.
     # A bucket is skipped when no lane has its two group bounds overlapping.
@@ -455,10 +477,8 @@ def _state_function(lay: RobotLayout, program) -> str:
         # is <= the threshold: one compare per obstacle
         emit(f"      const float4 bnd = p[{bound}];")
         emit(f"      const float brad = {radius.replace('pp[', 'p[')};")
-        for gi, grp in enumerate(groups):
-            mx, my, mz = _exyz(grp[len(grp) // 2])
-            w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
-            emit(f"      float wm{gi} = {w};" if gi == 0 else f"      wm0 = fminf(wm0, {w});")
+        for ti, w in enumerate(bound_terms()):
+            emit(f"      float wm0 = {w};" if ti == 0 else f"      wm0 = fminf(wm0, {w});")
         emit("      if (__any_sync(VMP_FULL, wm0 <= bnd.w)) {")
         group_tests(test_fn, coarse_fn, "        ")
         emit("      }")
@@ -483,10 +503,8 @@ def _state_function(lay: RobotLayout, program) -> str:
         emit(f"        const float brad = {radius};")
         # one compare per obstacle: the minimum over the groups of the expanded
         # bound distance (near iff some group's is <= the threshold)
-        for gi, grp in enumerate(groups):
-            mx, my, mz = _exyz(grp[len(grp) // 2])
-            w = f"vmp_sphere_w({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad)"
-            emit(f"        float wm{gi} = {w};" if gi == 0 else f"        wm0 = fminf(wm0, {w});")
+        for ti, w in enumerate(bound_terms()):
+            emit(f"        float wm0 = {w};" if ti == 0 else f"        wm0 = fminf(wm0, {w});")
         emit("        near = (near << 1) | (unsigned)(wm0 <= bnd.w);" if groups else "")
         emit("      }")
         emit("      unsigned todo = __reduce_or_sync(VMP_FULL, near);")

@@ -191,6 +191,46 @@ __device__ __forceinline__ bool vmp_clear_box(float x, float y, float z, float r
                    : vmp_clear_box_any(x, y, z, rs2, r0, r1, r2, r3);
 }
 
+/* ---------------------------------------------------------- packed FP32
+ * sm_100 executes fma.rn.f32x2 (FFMA2): two IEEE fused multiply-adds per lane
+ * in one instruction - the FMA pipe throughput is unchanged (measured 74.0 vs
+ * 70.7 TFLOP/s, scripts/exp_ffma2.cu) but it takes one issue slot instead of
+ * two.  Each half rounds exactly like a scalar fmaf, so packed results are
+ * bit-identical to the scalar forms. */
+typedef unsigned long long vmp_f2;
+
+__device__ __forceinline__ vmp_f2 vmp_pk(float lo, float hi) {
+  vmp_f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float vmp_lo(vmp_f2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float vmp_hi(vmp_f2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ vmp_f2 vmp_fma2(vmp_f2 a, vmp_f2 b, vmp_f2 c) {
+  vmp_f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+/* vmp_sphere_w of two broadphase groups (packed centres / S / -2R) against
+ * one obstacle bound, reduced with fminf: 4 FFMA2 + 1 FMNMX for two groups. */
+__device__ __forceinline__ float vmp_sphere_w2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2 S, vmp_f2 m2rs,
+                                               float4 r0, float r) {
+  vmp_f2 w = vmp_fma2(vmp_pk(r, r), m2rs, S);
+  w = vmp_fma2(x, vmp_pk(r0.x, r0.x), w);
+  w = vmp_fma2(y, vmp_pk(r0.y, r0.y), w);
+  w = vmp_fma2(z, vmp_pk(r0.z, r0.z), w);
+  return fminf(vmp_lo(w), vmp_hi(w));
+}
+
 /* Euclidean distance (broadphase group radii, inflated by the caller). */
 __device__ __forceinline__ float vmp_dist(float ax, float ay, float az, float bx, float by,
                                           float bz) {

@@ -17,6 +17,10 @@ cap() {  # cap <name> <kernel regex> <profile_kernels args...>
   python scripts/profile_kernels.py "$@" > gpurun_out/plain_$name.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"$re" -s 1 -c 1 \
       -o gpurun_out/prof_$name python scripts/profile_kernels.py "$@" > gpurun_out/ncu_$name.log 2>&1
+  # raw metrics as CSV (small); the .ncu-rep itself only where KEEP lists it
+  # (gpurun brings back at most 64 MiB)
+  ncu -i gpurun_out/prof_$name.ncu-rep --page raw --csv > gpurun_out/raw_$name.csv 2>/dev/null
+  if [[ " ${KEEP:-motion cfg1 cfg3} " != *" $name "* ]]; then rm -f gpurun_out/prof_$name.ncu-rep; fi
 }
 cap motion "vmp_motion_p" motion
 cap plan "plan_cluster" motion

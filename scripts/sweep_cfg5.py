@@ -7,11 +7,20 @@ TFLOP/s and fraction of the FP32 peak (SURVEY.md §8d F = 487 + 220 P), and
 the HBM traffic rate of the streamed batch.  Also times the FK-only kernel
 (HBM-bound).  One JSON object per line.
 
-    python scripts/sweep_cfg5.py > profiles/round1_sweep_cfg5.jsonl
+Every point records the SM clock and throttle reasons sampled (nvidia-smi,
+bench.ClockSampler) while its launches ran; fractions are of the FP32 peak
+MEASURED on the same GPU (bench.measure_fp32_peak, first line).  Points with
+N <= 2^18 are also timed "streamed": distinct resident batches (> 2x L2 in
+total) validated by one graph of PDL-chained launches (ConfigStream).
+"input_gbs" is algorithmic (4 dof + 1/8 byte per configuration / time), not
+measured DRAM traffic; ncu DRAM bytes for selected points are in profiles/.
+
+    python scripts/sweep_cfg5.py > profiles/round2_sweep_cfg5.jsonl
 """
 
 import json
 import sys
+import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -42,7 +51,9 @@ def timed(fn, reps=20, flush=None):
 
 def main():
     torch.cuda.set_device(0)
-    peak = bench.nominal_fp32_tflops()
+    peaks = bench.measure_fp32_peak(0)
+    peak = peaks["burst_tflops"]
+    print(json.dumps({"fp32_peak": peaks}), flush=True)
     hbm = 6539.9
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     rob = load_robot("arm7")
@@ -56,13 +67,28 @@ def main():
             q = qall[:, :n]
             out = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
             row = {"P": p, "N": n, "flop_per_config": f}
-            for mode, early in (("product", True), ("dense", False)):
-                ms = timed(lambda: ctx.validate_batch(q, early_exit=early, out=out), flush=flush)
-                rate = n / (ms / 1e3)
-                row[mode] = {"ms": round(ms, 4), "configs_per_s": round(rate, 1),
-                             "alg_tflops": round(rate * f / 1e12, 2),
-                             "frac_fp32": round(rate * f / 1e12 / peak, 4),
-                             "hbm_gbs": round(rate * (7 * 4 + 1 / 8) / 1e9, 1)}
+            with bench.ClockSampler(0) as clk:
+                for mode, early in (("product", True), ("dense", False)):
+                    ms = timed(lambda: ctx.validate_batch(q, early_exit=early, out=out), flush=flush)
+                    rate = n / (ms / 1e3)
+                    row[mode] = {"ms": round(ms, 4), "configs_per_s": round(rate, 1),
+                                 "alg_tflops": round(rate * f / 1e12, 2),
+                                 "frac_fp32": round(rate * f / 1e12 / peak, 4),
+                                 "input_gbs": round(rate * (7 * 4 + 1 / 8) / 1e9, 1)}
+                if n <= (1 << 18):
+                    copies = max(4, -(-2 * (126 << 20) // (7 * 4 * n)))
+                    cs = ctx.stream_validator(n, copies)
+                    for i in range(copies):
+                        cs.load(i, q)
+                    ms = timed(cs, reps=5, flush=flush) / copies
+                    rate = n / (ms / 1e3)
+                    row["streamed"] = {"ms": round(ms, 4), "configs_per_s": round(rate, 1),
+                                       "alg_tflops": round(rate * f / 1e12, 2),
+                                       "frac_fp32": round(rate * f / 1e12 / peak, 4),
+                                       "batches": copies}
+                    del cs
+                time.sleep(0.25)          # let the sampler see this point's load
+            row["clocks"] = clk.summary()
             if lg == 20:
                 v = runtime.unpack_bits(out.cpu().numpy(), n)
                 row["collision_rate"] = round(1 - float(v.mean()), 4)
