@@ -167,6 +167,12 @@ int vmp_validate_motions_host(const vmp_robot *robot, const vmp_env *env, const 
                               void *scratch, int64_t scratch_bytes, void *workspace,
                               int64_t workspace_bytes, void *stream);
 
+/* Zero-filled device memory on the current device (scratch / workspace for
+ * bindings without their own allocator, e.g. a ctypes module); 0 bytes gives
+ * NULL.  vmp_device_free(NULL) is a no-op. */
+int vmp_device_alloc(int64_t bytes, void **out);
+void vmp_device_free(void *ptr);
+
 /* FP32 FMA-pipe microbenchmark: `launches` back-to-back launches of a kernel
  * of 4 independent FFMA chains per thread (8 x 256-thread CTAs per SM,
  * 2 * 256 * iters flop per thread per launch), timed with CUDA events on a

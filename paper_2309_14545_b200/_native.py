@@ -48,7 +48,8 @@ EXPORTS = (
     "vmp_set_device", "vmp_device_info", "vmp_motion_workspace_bytes", "vmp_pair_clear",
     "vmp_knn", "vmp_nn_distances", "vmp_debug_motion_trace", "vmp_robot_home",
     "vmp_motion_states", "vmp_bench_ffma", "vmp_validate_host", "vmp_validate_host_scratch_bytes",
-    "vmp_validate_motions_host", "vmp_motions_host_scratch_bytes",
+    "vmp_validate_motions_host", "vmp_motions_host_scratch_bytes", "vmp_device_alloc",
+    "vmp_device_free",
 )
 VMP_KNN_MAX_K = 32
 VMP_KNN_MAX_DIM = 64
@@ -121,6 +122,8 @@ def lib() -> ctypes.CDLL:
         "vmp_validate_motions_host": ([vp, vp, vp, vp, c_i64, c_i64, c_dbl, c_i32, c_u32, vp, vp, vp,
                                        vp, c_i64, vp, c_i64, vp], ctypes.c_int),
         "vmp_motions_host_scratch_bytes": ([vp, c_i64], c_i64),
+        "vmp_device_alloc": ([c_i64, ctypes.POINTER(vp)], ctypes.c_int),
+        "vmp_device_free": ([vp], None),
         "vmp_bench_ffma": ([c_i64, c_i32, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)],
                            ctypes.c_int),
         "vmp_motion_states": ([vp, vp, c_i64, c_i32, c_i64, c_dbl, c_i32, c_u32, vp, vp, vp, vp],
