@@ -8,7 +8,7 @@ WANT="$*"
 if [ -z "$WANT" ] || [[ " $WANT " == *" launches "* ]]; then
   B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
   $B > gpurun_out/plain_bench.log 2>&1 && \
-    ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv \
+    ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
         --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
 fi
 cap() {  # cap <name> <kernel regex> <profile_kernels args...>

@@ -76,7 +76,7 @@ def main():
                                  "frac_fp32": round(rate * f / 1e12 / peak, 4),
                                  "input_gbs": round(rate * (7 * 4 + 1 / 8) / 1e9, 1)}
                 if n <= (1 << 18):
-                    copies = max(4, -(-2 * (126 << 20) // (7 * 4 * n)))
+                    copies = min(512, max(4, -(-2 * (126 << 20) // (7 * 4 * n))))
                     cs = ctx.stream_validator(n, copies)
                     for i in range(copies):
                         cs.load(i, q)
