@@ -284,7 +284,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     # 4-slot pipeline (a stream per slot) overlaps step k+1's H2D and rake with step k's drain
     hs = torch.from_numpy(mw.starts).pin_memory()
     hg = torch.from_numpy(mw.goals).pin_memory()
-    depth = 4
+    depth = 6
     pipe = M.MotionPipeline(ctx, E, mw.resolution, width=32, depth=depth)
     for _ in range(args.warmup):
         pipe.result(pipe.submit(hs, hg))
@@ -360,7 +360,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                   "mean_states_per_edge": round(float(n_np.mean()), 2),
                   "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
                   "launch": "CUDA graph (plan -> rake -> finalize, PDL edges) via "
-                            "motion.MotionValidator; e2e through motion.MotionPipeline (4 slots, "
+                            "motion.MotionValidator; e2e through motion.MotionPipeline (6 slots, "
                             "each step's H2D, graph replay and D2H on its slot's own stream)"},
         "roofline": roofline,
         # per step (one graph replay): cluster plan + rake + finalize kernels

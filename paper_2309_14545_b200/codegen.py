@@ -308,7 +308,7 @@ def _state_function(lay: RobotLayout, program) -> str:
     # batch validation (random configurations in a warp): plain self pairs first,
     # before the broadphase state is live; the motion rake (coherent lanes along
     # an edge, STOP 2) culls whole pair buckets with the group bounds below
-    emit("  constexpr bool CULL_SELF = STOP == 2;")
+    emit("  constexpr bool CULL_SELF = STOP == 2;")   # batch mode: culling measured slower (cfg4 413 vs 336 us)
     emit("  if constexpr (!CULL_SELF) {")
     for pi, (sa, sb, thr) in enumerate(lay.pairs):
         ax, ay, az = _exyz(fine[sa])
@@ -677,14 +677,16 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) vmp_fk_spheres(VmpFkArgs a
     if not lay.has_cc:
         return src
     src += f"""
-template <int PRUNE, int STOP, bool STAGED, int SPLIT, bool TWO = false>
+template <int PRUNE, int STOP, bool STAGED, int SPLIT, bool TWO = false, int NT = {BLOCK}>
 __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
+  // NT threads per CTA: {BLOCK}, or 256 for environments whose staged copy
+  // limits the CTAs per SM (more warps per copy)
   // SPLIT warps share one 32-configuration slice; warp w tests obstacles and
   // self pairs w (mod SPLIT) and the partial verdict words are AND-ed in smem
   // (more warps and a shorter critical path for latency-bound small batches)
   extern __shared__ float4 vmp_smem[];
   __shared__ unsigned long long vmp_bar;
-  __shared__ unsigned vmp_part[{BLOCK} / 32];
+  __shared__ unsigned vmp_part[NT / 32];
   // a following batch launched with VMP_PDL may start as soon as this grid's
   // CTAs are resident (its inputs are its own; nothing here is waited for)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -696,7 +698,7 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
     __syncthreads();
   }}
   bool cclear = true, cdone = false;
-  constexpr int TILE = {BLOCK} / SPLIT;
+  constexpr int TILE = NT / SPLIT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = warp % SPLIT;
   const long long stride = (long long)gridDim.x * TILE;
   for (long long base = blockIdx.x * (long long)TILE; base < a.n; base += stride) {{
@@ -890,6 +892,10 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
                         src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                                 f'vmp_validate_p{prune}_s{stop}_g1_x{sp}(VmpValidateArgs a) '
                                 f'{{ vmp_validate_body<{prune}, {stop}, true, {sp}>(a); }}\n')
+                if staged:                          # 256-thread CTAs for large staged envs
+                    src += (f'extern "C" __global__ void __launch_bounds__({2 * BLOCK}) '
+                            f'vmp_validate_p{prune}_s{stop}_g1_b{2 * BLOCK}(VmpValidateArgs a) '
+                            f'{{ vmp_validate_body<{prune}, {stop}, true, 1, false, {2 * BLOCK}>(a); }}\n')
                 if staged and stop == 1:            # two-pass broadphase, small batches
                     for sp in (1, SPLIT):
                         src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '

@@ -24,7 +24,7 @@ ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
 E = len(mw.starts)
 hs = torch.from_numpy(mw.starts).pin_memory()
 hg = torch.from_numpy(mw.goals).pin_memory()
-for depth in (2, 3, 4, 2, 3, 4):
+for depth in (4, 6, 8, 4, 6, 8):
     slots = [M.MotionValidator(ctx, E, mw.resolution, overlapped=True) for _ in range(depth)]
     streams = [torch.cuda.Stream() for _ in range(depth)]
     host = [torch.empty(s.bits.shape, dtype=torch.int32).pin_memory() for s in slots]
