@@ -527,16 +527,18 @@ def latency_summary(mw, rob, calls: int = 300) -> dict:
 # ------------------------------------------------------- CPU reference arm
 
 _CPU = {}
-# the reference package itself (pure Python / NumPy), staged git-ignored by
-# scripts/run_reference_suite.sh --stage; it travels to the GPU box with the repo
-REF_SRC = ROOT / "baseline" / "_ref" / "pkg" / "src"
+# the reference package itself (pure Python / NumPy), git-ignored, travels to the
+# GPU box with the repo: the offline pip install into baseline/_ref (DESIGN.md
+# §5), else the source tree staged by scripts/run_reference_suite.sh --stage
+REF_SRC = next((d for d in (ROOT / "baseline" / "_ref", ROOT / "baseline" / "_ref" / "pkg" / "src")
+                if (d / "vecmp" / "collision.py").is_file()), ROOT / "baseline" / "_ref")
 
 
 def _ref_context(mw):
     """The reference's own ValidationContext(width=8) for config 2: its bundled
     arm7 URDF / sphere model compiled by its own tracing compiler, the scene
     converted to its primitive types.  None when the package is not staged."""
-    if not (REF_SRC / "vecmp").is_dir():
+    if not (REF_SRC / "vecmp" / "collision.py").is_file():
         return None
     sys.path.insert(0, str(REF_SRC))
     import vecmp.collision as RC
