@@ -60,7 +60,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 30
+CODEGEN_VERSION = 31
 # packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
 FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
@@ -821,16 +821,14 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
       have = true;
     }}
-    long long ci, ei;
-    int n, chunks;
-    if (t < E) {{                            // round 0: edge t, discretised here
-      ci = 0;
+    long long ci, ei, ri = -1;
+    int n, chunks, fe = 0;
+    if (t < E) {{                            // round 0: edge t, discretised here; its
+      ci = 0;                               // first iteration can never be skipped
       ei = t;
       n = vmp_discretize_edge<{lay.dof}>(a.starts + ei * a.sld, a.goals + ei * a.sld, a.resolution);
       chunks = (int)vmp_rake_chunks((unsigned)n, Wu);
-      if (lane == 0) a.n_of[ei] = n;        // for the finalize kernel
     }} else {{
-      long long ri;
       if (t < split) {{
         ci = vmp_find_round_any(vmp_off[warp], a.off, n_off, t, lane);
         ri = t - (ci < VMP_OFF_CACHE ? vmp_off[warp][ci] : __ldcg(a.off + ci));
@@ -839,15 +837,16 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
         ci = (VMP_HBINS - 1) + u / n_big;
         ri = u - (ci - (VMP_HBINS - 1)) * n_big;
       }}
-      const int4 rank = __ldcg(a.order + ri);               // (edge, n, chunks, 0)
+      // (edge, n, chunks, failure record): one L2 round trip decides a skip
+      const int4 rank = __ldcg(a.order + ri);
       ei = rank.x;
       n = rank.y;
       chunks = rank.z;
+      fe = rank.w;                          // 0, or INT_MAX - first failing iteration
     }}
     if (ci >= chunks) continue;             // absent (only past the histogram)
     // the native width (W = 32: chunk c is iteration c + 1) skips the divisions
     const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
-    const int fe = __ldcg(a.fail_enc + ei);  // 0, or INT_MAX - first failing iteration
 {"    const unsigned long long t_start = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
     if (fe == 0 || 0x7fffffff - fe > (int)first_iter) {{   // else: cannot lower the count
       float s[{dofp}], g[{dofp}];
@@ -869,9 +868,17 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       const bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc,
                                                                   a.env.nb, inr && cclear);
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
-      if (bad && lane == 0) {{
-        const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
-        atomicMax(a.fail_enc + ei, 0x7fffffff - (int)it);
+      if (bad) {{                            // warp-uniform
+        if (ri < 0) {{
+          // a failing round-0 item records into the edge's rank record, which
+          // the plan kernel (usually long finished by now) writes
+          asm volatile("griddepcontrol.wait;" ::: "memory");
+          ri = __ldcg(a.rank_of + ei);
+        }}
+        if (lane == 0) {{
+          const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
+          atomicMax(&a.order[ri].w, 0x7fffffff - (int)it);
+        }}
       }}
     }}
 {_TRACE_BLOCK if TRACE_ITEMS else ""}

@@ -30,18 +30,19 @@ typedef struct {
   int pad_;
 } VmpValidateArgs;
 
-/* Motion workspace (zero-filled once by the caller; the per-edge arrays are
- * laid out by the capacity the workspace size implies, E_cap; every call
- * resets the queue counters before the rake starts and re-zeroes fail_enc of
- * its edges in finalize):
+/* Motion workspace (the per-edge arrays are laid out by the capacity the
+ * workspace size implies, E_cap; every call resets the queue counters before
+ * the rake starts and rewrites every per-edge record it reads):
  *   VmpMotionHeader
  *   unsigned hist[VMP_HBINS], fill[VMP_HBINS]   chunk-count histogram / scatter cursors
  *   long long off[VMP_HBINS]                    first work item of chunk round c
- *   int fail_enc[E_cap]                         per edge: INT_MAX - first failing
- *                                               iteration, 0 while none
- *   int n[E_cap], chunks[E_cap]                 per edge: discretisation count (rake
- *                                               round 0); chunks (multi-kernel plan)
- *   int4 order[E_cap]                           (edge, n, chunks, 0) by chunk count desc
+ *   int rank_of[E_cap]                          per edge: index of its rank record
+ *   int n[E_cap], chunks[E_cap]                 per edge: discretisation count and
+ *                                               chunks (multi-kernel plan only)
+ *   int4 order[E_cap]                           rank records (edge, n, chunks, failure
+ *                                               record) by chunk count descending; the
+ *                                               failure record is INT_MAX - first failing
+ *                                               iteration, 0 while none (atomicMax)
  * Work item t < E is round 0 of edge t (input order, no plan needed); item
  * E <= t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c, where
  * off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest edges
@@ -70,9 +71,11 @@ typedef struct {
   VmpEnvView env;
   VmpMotionHeader *hdr;
   const long long *off; /* first work item of each chunk round */
-  const int4 *order;    /* rank records (edge, n, chunks, 0), chunk count descending */
-  int *fail_enc;        /* per edge: INT_MAX - first failing iteration, 0 while none */
-  int *n_of;            /* per edge: discretisation count (written by round 0) */
+  int4 *order;          /* rank records (edge, n, chunks, failure record), chunk count
+                           descending; .w = INT_MAX - first failing iteration, 0 while none */
+  const int *rank_of;   /* per edge: index of its rank record (read by failing round-0
+                           items after the plan, and by finalize) */
+  int *pad_ptr_;        /* reserved */
   unsigned long long *trace; /* debug timeline (VMP_MOTION_TRACE), normally null:
                                 per CTA [entry, plan ready, warp 0-3 queue empty,
                                 exit, work items taken] in globaltimer ns */

@@ -361,24 +361,26 @@ __device__ __forceinline__ float vmp_lerp_exact(float s, float g, float t) {
 }
 
 /* Outputs of edges [tid0 + tid, ...) stepping by nthreads (whole warps):
- * verdict word by ballot, n and the W-lane rake block count; resets each
- * edge's failure record (INT_MAX - first failing iteration, 0 = none) for the
- * next call. */
+ * verdict word by ballot, n and the W-lane rake block count.  An edge's
+ * outcome lives in its rank record (edge, n, chunks, failure record) at
+ * order[rank_of[edge]]; the failure record is INT_MAX - first failing
+ * iteration, 0 = none (the plan rewrites every record each call). */
 __device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w);
-__device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width, const int *n_of,
-                                                   int *fail_enc, unsigned *bits, int *n_states,
+__device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width, const int *rank_of,
+                                                   const int4 *order, unsigned *bits, int *n_states,
                                                    int *blocks, long long tid0, long long nthreads,
                                                    int tid) {
   for (long long base = tid0; base < n_edges; base += nthreads) {
     const long long e = base + tid;
     const bool inr = e < n_edges;
-    const int fe = inr ? __ldcg(fail_enc + e) : 0;
+    int4 rec = make_int4(0, 0, 0, 1);
+    if (inr) rec = __ldcg(order + __ldcg(rank_of + e));
+    const int fe = rec.w;
     const bool ok = inr && fe == 0;
     const unsigned m = __ballot_sync(VMP_FULL, ok);
     if (inr) {
-      if (fe) fail_enc[e] = 0;
       if ((tid & 31) == 0) bits[e >> 5] = m;
-      const int n = __ldcg(n_of + e);
+      const int n = rec.y;
       if (n_states) n_states[e] = n;
       if (blocks) blocks[e] = ok ? (int)vmp_ceil_div((unsigned)n, (unsigned)width) : 0x7fffffff - fe;
     }
