@@ -60,9 +60,11 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 31
+CODEGEN_VERSION = 32
 # packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
 FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
+# experiment switches (comma-separated names in VMP_EXP at codegen; scripts/exp_*.sh)
+EXP = frozenset(x for x in __import__("os").environ.get("VMP_EXP", "").split(",") if x)
 # per-item debug timeline records in the rake (scripts/exp_motion_trace.py sets
 # this before codegen runs); off in production - they cost ~2 % of the step
 TRACE_ITEMS = __import__("os").environ.get("VMP_MOTION_TRACE_ITEMS", "") == "1"
@@ -326,6 +328,8 @@ def _state_function(lay: RobotLayout, program) -> str:
     # radius - one bound test per group per obstacle replaces one per sphere
     groups = [dyn[i:i + GROUP_SIZE] for i in range(0, len(dyn), GROUP_SIZE)]
     emit("  constexpr bool CULL = STOP != 0;")
+    emit(f"  constexpr bool VMP_WARP_VOTE = {'true' if 'warpvote' in EXP else 'false'};")
+    emit(f"  constexpr bool VMP_RAKE_VOTE = {'true' if 'rakevote' in EXP else 'false'};")
     for gi, grp in enumerate(groups):
         mid = grp[len(grp) // 2]
         mx, my, mz = _exyz(mid)
@@ -349,6 +353,66 @@ def _state_function(lay: RobotLayout, program) -> str:
         emit(f"  const vmp_f2 Q{gi}X = vmp_pk({ax}, {bx}), Q{gi}Y = vmp_pk({ay}, {by}), "
              f"Q{gi}Z = vmp_pk({az}, {bz});")
         emit(f"  const vmp_f2 Q{gi}S = vmp_pk(G{gi}S, G{gi + 1}S), Q{gi}M = vmp_pk(G{gi}M, G{gi + 1}M);")
+
+    # narrowphase units: two spheres per packed (FFMA2) test.  Only spheres
+    # whose three coordinates all depend on the configuration are paired: a constant
+    # coordinate (0 along an axis the sphere never leaves, e.g. a torso
+    # sphere) lets the compiler fold terms of the scalar form away, which a
+    # packed operand would carry as real work.  The rest stay scalar.
+    kinds_all = [int(k) for k in program.kinds]
+
+    def fully_dynamic(s):
+        return all(kinds_all[v] != CONST for v in s.xyz)
+    units: list[tuple] = []            # (sphere,) or (sphere_a, sphere_b)
+    if FFMA2 and "nopack" not in EXP:
+        # spheres of two adjacent groups pair position by position with the mids
+        # aligned: the mids' pair is then also the packed operand of the
+        # broadphase chain (one register pair serves both)
+        mate: dict[int, FineSphere] = {}
+        for gi in range(0, len(groups) - 1, 2):
+            a, b = groups[gi], groups[gi + 1]
+            ma, mb = len(a) // 2, len(b) // 2
+            for d in range(-GROUP_SIZE, GROUP_SIZE + 1):
+                if 0 <= ma + d < len(a) and 0 <= mb + d < len(b):
+                    sa, sb = a[ma + d], b[mb + d]
+                    if fully_dynamic(sa) and fully_dynamic(sb):
+                        mate[sa.slot], mate[sb.slot] = sb, sa
+        # leftover movers pair up in order
+        rest = [s for s in dyn if fully_dynamic(s) and s.slot not in mate]
+        for i in range(0, len(rest) - 1, 2):
+            mate[rest[i].slot], mate[rest[i + 1].slot] = rest[i + 1], rest[i]
+        seen: set = set()
+        for s in dyn:
+            if s.slot in seen:
+                continue
+            if s.slot in mate:
+                units.append((s, mate[s.slot]))
+                seen.update((s.slot, mate[s.slot].slot))
+            else:
+                units.append((s,))
+                seen.add(s.slot)
+    else:
+        units = [(s,) for s in dyn]
+    for ui, u in enumerate(units):
+        if len(u) == 2:
+            (ax, ay, az), (bx, by, bz) = _exyz(u[0]), _exyz(u[1])
+            emit(f"  const vmp_f2 P{ui}X = vmp_pk({ax}, {bx}), P{ui}Y = vmp_pk({ay}, {by}), "
+                 f"P{ui}Z = vmp_pk({az}, {bz});")
+            emit(f"  const vmp_f2 P{ui}S = vmp_pk(S{u[0].slot}, S{u[1].slot});")
+
+    def bound_masks(ind: str) -> None:
+        """Per obstacle: shift every group's near bit into its per-lane mask."""
+        paired = set()
+        for _, gi in pairs:
+            emit(ind + f"{{ const vmp_f2 w = vmp_near2(Q{gi}X, Q{gi}Y, Q{gi}Z, Q{gi}S, Q{gi}M, bnd, brad); "
+                 f"n{gi} = vmp_push_sign(n{gi}, vmp_lo(w)); "
+                 f"n{gi + 1} = vmp_push_sign(n{gi + 1}, vmp_hi(w)); }}")
+            paired.update((gi, gi + 1))
+        for gi, grp in enumerate(groups):
+            if gi not in paired:
+                mx, my, mz = _exyz(grp[len(grp) // 2])
+                emit(ind + f"n{gi} = vmp_push_sign(n{gi}, "
+                     f"vmp_near1({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad));")
 
     def bound_terms() -> list[str]:
         """Per obstacle: the expanded bound distance of every group, as terms
@@ -412,22 +476,36 @@ def _state_function(lay: RobotLayout, program) -> str:
     for s in dyn:
         by_link.setdefault(s.link, []).append(s)
 
+    def pruned(s):
+        return s.link in coarse_links and len(by_link[s.link]) >= 2
+    # per-link coarse prune (reference collision.py:367-381): in dense mode only,
+    # unless VMP_EXP=coarse - the group broadphase already culls per 3 spheres
+    prune_expr = "PRUNE" if "coarse" in EXP else "(PRUNE && !CULL)"
+    pruned_links = sorted({s.link for u in units if all(pruned(x) for x in u) for s in u})
+
     def group_tests(test_fn, coarse_fn, ind: str = "    ") -> None:
-        for link, spheres in by_link.items():
-            tests = [test_fn(s) for s in spheres]
-            if link in coarse_links and len(spheres) >= 2:
-                emit(ind + "if (!PRUNE || __any_sync(VMP_FULL, !" + coarse_fn(link) + ")) {")
-                for t in tests:
-                    emit(ind + "  ok &= " + t + ";")
-                emit(ind + "}")
+        """Every narrowphase unit against the obstacle record in r0..r3.  A
+        unit whose spheres all sit on links with a coarse sphere (>= 2 fine
+        spheres) is skipped when every lane's coarse spheres are clear; each
+        link's coarse vote is taken once per obstacle."""
+        for link in pruned_links:
+            emit(ind + f"const bool near{link} = !{prune_expr} || "
+                 f"__any_sync(VMP_FULL, !{coarse_fn(link)});")
+        for ui, u in enumerate(units):
+            test = test_fn(u[0]) if len(u) == 1 else test_fn(u[0], u[1], ui)
+            if all(pruned(s) for s in u):
+                cond = " || ".join(f"near{link}" for link in sorted({s.link for s in u}))
+                emit(ind + f"if ({cond}) ok &= {test};")
             else:
-                for t in tests:
-                    emit(ind + "ok &= " + t + ";")
+                emit(ind + f"ok &= {test};")
 
     def coarse_xyz(link):
         return lay.coarse[link][0], coarse_env[link]
 
-    def sph_test(s):
+    def sph_test(s, s2=None, ui=None):
+        if s2 is not None:
+            return (f"vmp_clear_sphere2(P{ui}X, P{ui}Y, P{ui}Z, P{ui}S, {f32_literal(2.0 * np.float32(s.radius))}, "
+                    f"{f32_literal(2.0 * np.float32(s2.radius))}, r0, r1.x)")
         x, y, z = _exyz(s)
         return f"vmp_clear_sphere({x}, {y}, {z}, S{s.slot}, {f32_literal(-2.0 * np.float32(s.radius))}, r0, r1.x)"
 
@@ -437,7 +515,10 @@ def _state_function(lay: RobotLayout, program) -> str:
         return (f"vmp_clear_sphere({x}, {y}, {z}, vmp_sphere_S({x}, {y}, {z}, {f32_literal(rs2)}), "
                 f"{f32_literal(-2.0 * np.float32(r))}, r0, r1.x)")
 
-    def cap_test(s):
+    def cap_test(s, s2=None, ui=None):
+        if s2 is not None:
+            return (f"vmp_clear_capsule2(P{ui}X, P{ui}Y, P{ui}Z, P{ui}S, {f32_literal(2.0 * np.float32(s.radius))}, "
+                    f"{f32_literal(2.0 * np.float32(s2.radius))}, r0, r1, r2)")
         x, y, z = _exyz(s)
         return f"vmp_clear_capsule({x}, {y}, {z}, S{s.slot}, {f32_literal(-2.0 * np.float32(s.radius))}, r0, r1, r2)"
 
@@ -450,7 +531,13 @@ def _state_function(lay: RobotLayout, program) -> str:
     def box_fn(radius):
         return "vmp_clear_box_small" if radius < 1.0 else "vmp_clear_box_any"
 
-    def box_test(s):
+    def box_test(s, s2=None, ui=None):
+        if s2 is not None:
+            ra2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
+            rb2 = np.float32(np.float32(s2.radius) * np.float32(s2.radius))
+            small = lambda r: "true" if r < 1.0 else "false"
+            return (f"vmp_clear_box2<{small(s.radius)}, {small(s2.radius)}>(P{ui}X, P{ui}Y, P{ui}Z, "
+                    f"{f32_literal(ra2)}, {f32_literal(rb2)}, r0, r1, r2, r3)")
         x, y, z = _exyz(s)
         rs2 = np.float32(np.float32(s.radius) * np.float32(s.radius))
         return f"{box_fn(s.radius)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
@@ -469,8 +556,42 @@ def _state_function(lay: RobotLayout, program) -> str:
         emit(f"      const float4 {loads};")
         group_tests(test_fn, coarse_fn, "      ")
         emit("    }")
+        emit("  } else if constexpr (TWO ? !VMP_RAKE_VOTE : !VMP_WARP_VOTE) {")
+        # batch validation (unrelated configurations in a warp): per-lane near
+        # lists.  Pass 1 tests every group bound against every obstacle bound
+        # of a 32-obstacle chunk into one bit mask per group per lane; pass 2
+        # walks the groups and each lane pops ITS OWN near obstacles, testing
+        # only that group's spheres (per-lane record address).  A warp vote
+        # here would call an obstacle near when any of 32 unrelated
+        # configurations is (35-50 % of obstacles on configs 1 / 3 / 4) and
+        # make every lane test every sphere; the lists cut the sphere tests
+        # 4-8x (scripts/exp_lane_cull_model.py).  A lane whose verdict is
+        # already false drops its lists.
+        emit(f"    for (int k0 = sub; k0 < {count}; k0 += 32 * split, p += 32 * split * {f4}) {{")
+        emit(f"      const int kn = min(32, ({count} - k0 + split - 1) / split);")
+        emit("      unsigned " + ", ".join(f"n{gi} = 0" for gi in range(len(groups))) + ";")
+        emit(f"      const float4 *pp = p + (kn - 1) * split * {f4};")
+        emit("#pragma unroll 2")
+        emit(f"      for (int j = kn - 1; j >= 0; --j, pp -= split * {f4}) {{")
+        emit(f"        const float4 bnd = pp[{bound}];")
+        emit(f"        const float brad = {radius};")
+        bound_masks("        ")
+        emit("      }")
+        for gi, grp in enumerate(groups):
+            emit(f"      while (n{gi} != 0 && ok) {{")
+            emit(f"        const int j = __ffs(n{gi}) - 1;")
+            emit(f"        n{gi} &= n{gi} - 1;")
+            emit(f"        const float4 *pq = p + j * split * {f4};")
+            emit(f"        const float4 {loads.replace('p[', 'pq[')};")
+            for sph in grp:
+                emit(f"        ok &= {test_fn(sph)};")
+            emit("      }")
+            # the rake stops at the first invalid state of the chunk
+            emit("      if (STOP == 2 && VMP_STOP_NOW) return ok;")
+        emit("      if (STOP == 1 && VMP_STOP_NOW) return ok;")
+        emit("    }")
         emit("  } else if constexpr (STOP == 1 && !TWO) {")
-        # batch validation: one pass, a warp vote per obstacle on the group bounds
+        # warp-vote variant (VMP_EXP=warpvote): one pass, a vote per obstacle
         emit(f"    for (int k = sub; k < {count}; k += split, p += split * {f4}) {{")
         emit(f"      const float4 {loads};")
         # near iff the minimum over the groups of the expanded bound distance

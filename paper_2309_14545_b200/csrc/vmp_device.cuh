@@ -121,8 +121,8 @@ __device__ __forceinline__ const float4 *vmp_env_begin(const VmpEnvView &env, in
  * + r; cuboid: centre, |h|; both + 1e-5 m), tested like a sphere obstacle for
  * the warp-level broadphase cull of the generated kernels.
  * For a robot sphere with centre c and radius rs, S = |c|^2 - rs^2 and
- *   |c - o|^2 - (r + rs)^2 = S + r (-2 rs) + (-2 o).c + (|o|^2 - r^2)
- * so the sphere test is 4 FFMA + 1 FSETP.  Hit <=> value <= 0, i.e. boundary
+ *   |c - o|^2 - (r + rs)^2 = S + (-2 o).c + (|o|^2 - r^2) - 2 rs r
+ * so the sphere test is 4 FFMA + 1 FSETP: S + (-2 o).c > 2 rs r - (|o|^2 - r^2).  Hit <=> value <= 0, i.e. boundary
  * contact counts as collision (reference collision.py:5-6, 206-211).
  */
 
@@ -139,24 +139,24 @@ __device__ __forceinline__ float vmp_sphere_w(float x, float y, float z, float S
 /* true = clear (no contact) */
 __device__ __forceinline__ bool vmp_clear_sphere(float x, float y, float z, float S, float m2rs,
                                                  float4 r0, float r) {
-  float w = fmaf(r, m2rs, S);
-  w = fmaf(x, r0.x, w);
+  /* the radius cross term sits on the compare side, as in the packed
+   * two-sphere form (vmp_clear_sphere2), which must agree bit for bit */
+  float w = fmaf(x, r0.x, S);
   w = fmaf(y, r0.y, w);
   w = fmaf(z, r0.z, w);
-  return w > r0.w;
+  return w > fmaf(r, -m2rs, r0.w);
 }
 
 __device__ __forceinline__ bool vmp_clear_capsule(float x, float y, float z, float S, float m2rs,
                                                   float4 r0, float4 r1, float4 r2) {
   float u = fmaf(x, r0.x, fmaf(y, r0.y, fmaf(z, r0.z, r0.w)));  /* (c - p0).a */
   float t = __saturatef(u * r2.x);                                /* clamp(u / |a|^2, 0, 1) */
-  float w = fmaf(r2.z, m2rs, S);
-  w = fmaf(x, r1.x, w);
+  float w = fmaf(x, r1.x, S);
   w = fmaf(y, r1.y, w);
-  w = fmaf(z, r1.z, w);                                            /* |c - p0|^2 - thr - A */
+  w = fmaf(z, r1.z, w);                                            /* |c - p0|^2 - rs^2 - A */
   float v = fmaf(u, -2.0f, t * r2.y);                              /* t |a|^2 - 2 u */
-  float e = fmaf(t, v, w);                                         /* |c - p0 - t a|^2 - thr - A */
-  return e > r1.w;
+  float e = fmaf(t, v, w);                                         /* |c - p0 - t a|^2 - rs^2 - A */
+  return e > fmaf(r2.z, -m2rs, r1.w);                              /* + 2 rs r: vs (r + rs)^2 */
 }
 
 /* rs < 1: |l| - h saturated to [0, 1] is exact below 1 and >= rs^2 above, so
@@ -229,6 +229,95 @@ __device__ __forceinline__ float vmp_sphere_w2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp
   w = vmp_fma2(y, vmp_pk(r0.y, r0.y), w);
   w = vmp_fma2(z, vmp_pk(r0.z, r0.z), w);
   return fminf(vmp_lo(w), vmp_hi(w));
+}
+
+__device__ __forceinline__ vmp_f2 vmp_mul2(vmp_f2 a, vmp_f2 b) {
+  vmp_f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ vmp_f2 vmp_add2(vmp_f2 a, vmp_f2 b) {
+  vmp_f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+/* a scalar in both halves: FFMA2 takes it as a broadcast operand (Rn.F32), no MOV */
+__device__ __forceinline__ vmp_f2 vmp_bc(float s) { return vmp_pk(s, s); }
+
+/* Narrowphase tests of TWO robot spheres (packed centres x / y / z, S and
+ * -2 rs) against one obstacle record: each half evaluates exactly the scalar
+ * form above with IEEE fma per half (sphere / capsule: the radius cross term
+ * moved to the compare side), at ~0.65 of the issue slots (sphere 3 FFMA2 +
+ * 2 FFMA + 2 FSETP; capsule 9 packed + 2 FMUL.SAT + 2 FFMA + 2 FSETP; cuboid
+ * 12 packed + 6 FADD.SAT + 2 FSETP).  true = both spheres clear. */
+__device__ __forceinline__ bool vmp_clear_sphere2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2 S,
+                                                  float rsa2, float rsb2, float4 r0, float r) {
+  /* the radius cross term 2 rs r sits on the compare side (one scalar FFMA
+   * with an immediate per sphere): no packed per-sphere constants */
+  vmp_f2 w = vmp_fma2(x, vmp_bc(r0.x), S);
+  w = vmp_fma2(y, vmp_bc(r0.y), w);
+  w = vmp_fma2(z, vmp_bc(r0.z), w);
+  return (vmp_lo(w) > fmaf(r, rsa2, r0.w)) & (vmp_hi(w) > fmaf(r, rsb2, r0.w));
+}
+
+__device__ __forceinline__ bool vmp_clear_capsule2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2 S,
+                                                   float rsa2, float rsb2, float4 r0, float4 r1,
+                                                   float4 r2) {
+  const vmp_f2 u = vmp_fma2(x, vmp_bc(r0.x), vmp_fma2(y, vmp_bc(r0.y),
+                            vmp_fma2(z, vmp_bc(r0.z), vmp_bc(r0.w))));
+  const vmp_f2 t = vmp_pk(__saturatef(vmp_lo(u) * r2.x), __saturatef(vmp_hi(u) * r2.x));
+  vmp_f2 w = vmp_fma2(x, vmp_bc(r1.x), S);
+  w = vmp_fma2(y, vmp_bc(r1.y), w);
+  w = vmp_fma2(z, vmp_bc(r1.z), w);
+  const vmp_f2 v = vmp_fma2(u, vmp_bc(-2.0f), vmp_mul2(t, vmp_bc(r2.y)));
+  const vmp_f2 e = vmp_fma2(t, v, w);
+  return (vmp_lo(e) > fmaf(r2.z, rsa2, r1.w)) & (vmp_hi(e) > fmaf(r2.z, rsb2, r1.w));
+}
+
+template <bool SMALL_A, bool SMALL_B>
+__device__ __forceinline__ bool vmp_clear_box2(vmp_f2 x, vmp_f2 y, vmp_f2 z, float rs2a, float rs2b,
+                                               float4 r0, float4 r1, float4 r2, float4 r3) {
+  const vmp_f2 l0 = vmp_fma2(x, vmp_bc(r0.x), vmp_fma2(y, vmp_bc(r0.y),
+                             vmp_fma2(z, vmp_bc(r0.z), vmp_bc(r0.w))));
+  const vmp_f2 l1 = vmp_fma2(x, vmp_bc(r1.x), vmp_fma2(y, vmp_bc(r1.y),
+                             vmp_fma2(z, vmp_bc(r1.z), vmp_bc(r1.w))));
+  const vmp_f2 l2 = vmp_fma2(x, vmp_bc(r2.x), vmp_fma2(y, vmp_bc(r2.y),
+                             vmp_fma2(z, vmp_bc(r2.z), vmp_bc(r2.w))));
+  /* rs < 1: FADD.SAT (see vmp_clear_box_small); else FADD + FMNMX */
+#define VMP_EXC(SMALL, l, h) (SMALL ? __saturatef(fabsf(l) - (h)) : fmaxf(fabsf(l) - (h), 0.0f))
+  const vmp_f2 e0 = vmp_pk(VMP_EXC(SMALL_A, vmp_lo(l0), r3.x), VMP_EXC(SMALL_B, vmp_hi(l0), r3.x));
+  const vmp_f2 e1 = vmp_pk(VMP_EXC(SMALL_A, vmp_lo(l1), r3.y), VMP_EXC(SMALL_B, vmp_hi(l1), r3.y));
+  const vmp_f2 e2 = vmp_pk(VMP_EXC(SMALL_A, vmp_lo(l2), r3.z), VMP_EXC(SMALL_B, vmp_hi(l2), r3.z));
+#undef VMP_EXC
+  const vmp_f2 d = vmp_fma2(e0, e0, vmp_fma2(e1, e1, vmp_mul2(e2, e2)));
+  return (vmp_lo(d) > rs2a) & (vmp_hi(d) > rs2b);
+}
+
+/* Per-lane near masks of the batch kernels: the expanded bound distance minus
+ * its threshold, whose SIGN BIT is the near flag (shifted into a mask with one
+ * funnel shift).  "near" = strictly negative: a real contact makes the exact
+ * value <= -(the bounds' inflation margins), far beyond the rounding of these
+ * sums, so treating an exact 0 as clear cannot drop a contact. */
+__device__ __forceinline__ vmp_f2 vmp_sub2(vmp_f2 a, vmp_f2 b) {
+  vmp_f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ vmp_f2 vmp_near2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2 S, vmp_f2 m2rs,
+                                            float4 r0, float r) {
+  vmp_f2 w = vmp_fma2(vmp_bc(r), m2rs, vmp_sub2(S, vmp_bc(r0.w)));
+  w = vmp_fma2(x, vmp_bc(r0.x), w);
+  w = vmp_fma2(y, vmp_bc(r0.y), w);
+  w = vmp_fma2(z, vmp_bc(r0.z), w);
+  return w;
+}
+__device__ __forceinline__ float vmp_near1(float x, float y, float z, float S, float m2rs,
+                                           float4 r0, float r) {
+  return fmaf(z, r0.z, fmaf(y, r0.y, fmaf(x, r0.x, fmaf(r, m2rs, S - r0.w))));
+}
+/* mask = (mask << 1) | sign(w) */
+__device__ __forceinline__ unsigned vmp_push_sign(unsigned mask, float w) {
+  return __funnelshift_l(__float_as_uint(w), mask, 1);
 }
 
 /* Euclidean distance (broadphase group radii, inflated by the caller). */
