@@ -311,13 +311,6 @@ def _state_function(lay: RobotLayout, program) -> str:
     # before the broadphase state is live; the motion rake (coherent lanes along
     # an edge, STOP 2) culls whole pair buckets with the group bounds below
     emit("  constexpr bool CULL_SELF = STOP == 2;")   # batch mode: culling measured slower (cfg4 413 vs 336 us)
-    emit("  if constexpr (!CULL_SELF) {")
-    for pi, (sa, sb, thr) in enumerate(lay.pairs):
-        ax, ay, az = _exyz(fine[sa])
-        bx, by, bz = _exyz(fine[sb])
-        emit(f"    if (sub == {pi} % split) "
-             f"ok &= vmp_clear_pair({bx}, {by}, {bz}, {ax}, {ay}, {az}, {f32_literal(thr)});")
-    emit("  }")
     # per-sphere constants
     for s in dyn:
         x, y, z = _exyz(s)
@@ -330,6 +323,8 @@ def _state_function(lay: RobotLayout, program) -> str:
     emit("  constexpr bool CULL = STOP != 0;")
     emit(f"  constexpr bool VMP_WARP_VOTE = {'true' if 'warpvote' in EXP else 'false'};")
     emit(f"  constexpr bool VMP_RAKE_VOTE = {'true' if 'rakevote' in EXP else 'false'};")
+    main_emit, group_lines = emit, []
+    emit = group_lines.append          # group bounds are emitted after the batch self pairs
     for gi, grp in enumerate(groups):
         mid = grp[len(grp) // 2]
         mx, my, mz = _exyz(mid)
@@ -353,6 +348,7 @@ def _state_function(lay: RobotLayout, program) -> str:
         emit(f"  const vmp_f2 Q{gi}X = vmp_pk({ax}, {bx}), Q{gi}Y = vmp_pk({ay}, {by}), "
              f"Q{gi}Z = vmp_pk({az}, {bz});")
         emit(f"  const vmp_f2 Q{gi}S = vmp_pk(G{gi}S, G{gi + 1}S), Q{gi}M = vmp_pk(G{gi}M, G{gi + 1}M);")
+    emit = main_emit
 
     # narrowphase units: two spheres per packed (FFMA2) test.  Only spheres
     # whose three coordinates all depend on the configuration are paired: a constant
@@ -399,6 +395,65 @@ def _state_function(lay: RobotLayout, program) -> str:
             emit(f"  const vmp_f2 P{ui}X = vmp_pk({ax}, {bx}), P{ui}Y = vmp_pk({ay}, {by}), "
                  f"P{ui}Z = vmp_pk({az}, {bz});")
             emit(f"  const vmp_f2 P{ui}S = vmp_pk(S{u[0].slot}, S{u[1].slot});")
+
+    # batch validation (unrelated configurations in a warp): every self pair, in
+    # expanded form |a|^2 + |b|^2 - 2 a.b against thr - ra^2 - rb^2 (S = |c|^2 -
+    # rs^2 is shared with the obstacle tests), two partners of one sphere per
+    # packed chain when they share a narrowphase unit: 3 issue slots per pair
+    # instead of 7 (config 4 carries 267 pairs per configuration).  Before the
+    # group bounds are live.  The rake (STOP 2) culls pair buckets instead.
+    vals = np.asarray(program.values, dtype=np.float64)
+
+    def rs2_of(sp):
+        return np.float32(np.float32(sp.radius) * np.float32(sp.radius))
+
+    def s_expr(sp):
+        if not sp.const:
+            return f"S{sp.slot}"
+        c = np.asarray([np.float32(vals[v] - o) for v, o in zip(sp.xyz, lay.home)], dtype=np.float64)
+        return f32_literal(float(c @ c) - float(rs2_of(sp)))
+
+    def t_lit(sa, sb, thr):
+        return f32_literal(float(np.float32(thr)) - float(rs2_of(fine[sa])) - float(rs2_of(fine[sb])))
+    # the pair relation is symmetric: sphere c broadcasts (-2 c, S_c) and every
+    # unit whose two spheres are both partners of c takes one packed test
+    thr_of = {frozenset((sa, sb)): thr for sa, sb, thr in lay.pairs}
+    nbrs: dict[int, set] = {}
+    for sa, sb, _ in lay.pairs:
+        nbrs.setdefault(sa, set()).add(sb)
+        nbrs.setdefault(sb, set()).add(sa)
+    todo = set(thr_of)
+    plan: dict[int, list] = {}
+    for c in sorted(nbrs, key=lambda c: -len(nbrs[c])):
+        for ui, u in enumerate(units):
+            if len(u) == 2 and all(frozenset((sp.slot, c)) in todo for sp in u):
+                plan.setdefault(c, []).append(("pk", ui))
+                todo -= {frozenset((sp.slot, c)) for sp in u}
+    for pair in sorted(todo, key=sorted):
+        sa, sb = sorted(pair)
+        c = sb if sb in plan or sa not in plan else sa
+        plan.setdefault(c, []).append(("one", sa if c == sb else sb))
+    emit("  if constexpr (!CULL_SELF) {")
+    ti = 0
+    for c, tests in plan.items():
+        bx, by, bz = _exyz(fine[c])
+        emit(f"    {{ const float mx = -2.0f * {bx}, my = -2.0f * {by}, mz = -2.0f * {bz}, "
+             f"sb = {s_expr(fine[c])};")
+        for kind, x in tests:
+            if kind == "pk":
+                u0, u1 = units[x]
+                emit(f"      if (sub == {ti} % split) ok &= vmp_clear_pair2(P{x}X, P{x}Y, P{x}Z, P{x}S, "
+                     f"mx, my, mz, sb, {t_lit(u0.slot, c, thr_of[frozenset((u0.slot, c))])}, "
+                     f"{t_lit(u1.slot, c, thr_of[frozenset((u1.slot, c))])});")
+            else:
+                ax, ay, az = _exyz(fine[x])
+                emit(f"      if (sub == {ti} % split) ok &= vmp_clear_pair_x({ax}, {ay}, {az}, "
+                     f"{s_expr(fine[x])}, mx, my, mz, sb, {t_lit(x, c, thr_of[frozenset((x, c))])});")
+            ti += 1
+        emit("    }")
+    emit("  }")
+    for line in group_lines:
+        emit(line)
 
     def bound_masks(ind: str) -> None:
         """Per obstacle: shift every group's near bit into its per-lane mask."""

@@ -339,6 +339,25 @@ __device__ __forceinline__ bool vmp_clear_pair(float ax, float ay, float az, flo
   return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) > thr;
 }
 
+/* Self pairs in expanded form (batch kernels): with S = |c|^2 - rs^2 of both
+ * spheres, |a - b|^2 > thr  <=>  Sa + Sb - 2 a.b > thr - ra^2 - rb^2 =: T
+ * (T a compile-time constant; (mx, my, mz) = -2 b).  The sums stay below a few
+ * m^2 in the robot's frame, so the rounding (~5e-7 m^2) moves a verdict only
+ * within ~3e-6 m of contact. */
+__device__ __forceinline__ bool vmp_clear_pair_x(float ax, float ay, float az, float sa, float mx,
+                                                 float my, float mz, float sb, float T) {
+  return fmaf(ax, mx, fmaf(ay, my, fmaf(az, mz, sa + sb))) > T;
+}
+/* two partners (packed centres and S) of one sphere b */
+__device__ __forceinline__ bool vmp_clear_pair2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2 S, float mx,
+                                                float my, float mz, float sb, float Ta, float Tb) {
+  vmp_f2 w = vmp_add2(S, vmp_bc(sb));
+  w = vmp_fma2(z, vmp_bc(mz), w);
+  w = vmp_fma2(y, vmp_bc(my), w);
+  w = vmp_fma2(x, vmp_bc(mx), w);
+  return (vmp_lo(w) > Ta) & (vmp_hi(w) > Tb);
+}
+
 /* Test one robot sphere against obstacle k (records ordered spheres, capsules, boxes). */
 __device__ __forceinline__ bool vmp_sphere_clear_obstacle(const float4 *rec, int ns, int nc, int nb,
                                                           int k, float x, float y, float z,
