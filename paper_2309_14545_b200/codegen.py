@@ -60,7 +60,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 32
+CODEGEN_VERSION = 37
 # packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
 FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
 # experiment switches (comma-separated names in VMP_EXP at codegen; scripts/exp_*.sh)
@@ -722,13 +722,15 @@ _FK_BODY_PLACEHOLDER = ["  VMP_FK_BODY"]
 def _const_check(lay: RobotLayout) -> str:
     """Per-CTA test of configuration-independent spheres against the env."""
     consts = lay.const_spheres
-    lines = ["__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb) {",
-             "  (void)env; (void)ns; (void)nc; (void)nb;",
+    lines = ["// tid of nth cooperating threads (the CTA, or one warp of the rake)",
+             "__device__ __forceinline__ bool vmp_const_clear(const float4 *env, int ns, int nc, int nb,",
+             "                                                int tid, int nth) {",
+             "  (void)env; (void)ns; (void)nc; (void)nb; (void)tid; (void)nth;",
              "  bool ok = true;"]
     if consts:
-        # (const sphere, obstacle) pairs spread over the CTA's threads
+        # (const sphere, obstacle) pairs spread over the cooperating threads
         lines.append("  const int nobst = ns + nc + nb;")
-        lines.append(f"  for (int t = threadIdx.x; t < {len(consts)} * nobst; t += blockDim.x) {{")
+        lines.append(f"  for (int t = tid; t < {len(consts)} * nobst; t += nth) {{")
         lines.append("    const int k = t % nobst;")
         lines.append("    switch (t / nobst) {")
         for k, s in enumerate(consts):
@@ -887,7 +889,8 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
                                                SPLIT, STAGED ? &vmp_bar : nullptr);
     if (!cdone) {{                            // CTA-uniform: once, after the first tile
       if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
-      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+      cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb,
+                                                   threadIdx.x, blockDim.x));
       cdone = true;
     }}
     ok = ok && cclear;
@@ -930,14 +933,18 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   // the finalize kernel may launch now: its CTAs fill SM slots as rake CTAs
   // retire and wait (griddepcontrol.wait) for this whole grid
   asm volatile("griddepcontrol.launch_dependents;");
+  // the environment copy overlaps the first item's queue atomic, edge loads,
+  // interpolation, FK and self pairs: vmp_state waits for it before the first
+  // obstacle, and each warp checks the constant spheres once, after its first
+  // item (a warp-level vote: no CTA barrier inside the item loop)
   const float4 *env = a.env.rec;
   if (STAGED) {{
     vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
-    __syncthreads();
-    vmp_mbar_wait(&vmp_bar, 0);
-    env = vmp_smem;
+    __syncthreads();                         // the mbarrier is initialised
+    env = vmp_smem;{"""
+    vmp_mbar_wait(&vmp_bar, 0);              // VMP_EXP=waitenv: no overlap (A/B)""" if "waitenv" in EXP else ""}
   }}
-  const bool cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb));
+  bool cclear = true, cdone = false;
   if (trace && threadIdx.x == 0) trace[1] = vmp_gtime();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long E = a.n_edges;
@@ -1041,8 +1048,15 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
       float q[{dofp}];
 #pragma unroll
       for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
-      const bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc,
-                                                                  a.env.nb, inr && cclear);
+      bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc, a.env.nb,
+                                                            inr && cclear, 0, 1,
+                                                            STAGED ? &vmp_bar : nullptr);
+      if (!cdone) {{                         // warp-uniform: once, after the first item
+        if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
+        cclear = __all_sync(VMP_FULL, vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, lane, 32));
+        cdone = true;
+        ok = ok && cclear;
+      }}
       const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
       if (bad) {{                            // warp-uniform
         if (ri < 0) {{
@@ -1060,6 +1074,193 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
 {_TRACE_BLOCK if TRACE_ITEMS else ""}
 
   }}
+  if (STAGED && !cdone) vmp_mbar_wait(&vmp_bar, 0);   // no item evaluated: still retire the copy
+  if (trace && threadIdx.x == 0) trace[6] = vmp_gtime();
+}}
+
+template <int PRUNE, int STOP, bool STAGED, bool NO_SPH = false>
+__device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
+  // Dynamic-queue rake (csrc/vmp_abi.h).  Round 0 - the first chunk of every
+  // edge, discretised by the item itself - is dealt out statically (warp w
+  // takes edges w, w + warps, ...): no atomics, nothing to wait for.  An edge
+  // whose first iteration passed publishes its remaining chunks as slot
+  // records; afterwards warps pop slots until the queue is drained.  Failed
+  // edges never enter the queue, nothing is planned or sorted.  Per queue item:
+  // one atomic (the next one issued before the current chunk is evaluated), one
+  // L2 round trip for the slot (its two words carry the call's tag: valid as
+  // soon as they read back), one for the edge rows and the failure record.
+  extern __shared__ float4 vmp_smem[];
+  __shared__ unsigned long long vmp_bar;
+  unsigned long long *trace = a.trace ? a.trace + 8 * blockIdx.x : nullptr;
+  if (trace && threadIdx.x == 0) trace[0] = vmp_gtime();
+  asm volatile("griddepcontrol.launch_dependents;");
+  const float4 *env = a.env.rec;
+  if (STAGED) {{
+    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
+    __syncthreads();                         // the mbarrier is initialised
+    env = vmp_smem;
+  }}
+  bool cclear = true, cdone = false;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long E = a.n_edges, cap = a.slot_cap;
+  const unsigned Wu = (unsigned)a.width;
+  unsigned long long *const state = a.dq + VMP_DQ_STATE;
+  constexpr unsigned long long M40 = (1ull << 40) - 1;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  (void)warp;
+  const long long guard = (long long)a.guard_waves * nwarps;
+  // vmp_k_motion_begin resets the queue words, zeroes fail[] and sets the call
+  // count: waited for (programmatic dependent launch) before the first write
+  // to any of them, i.e. after the first round-0 chunk has been evaluated
+  unsigned long long tag = 0;                // 0: the begin kernel has not been waited for
+  unsigned taken = 0;
+  unsigned long long grab = 0;
+  bool have = false;
+  long long r0 = wid;                        // next round-0 edge of this warp
+  int stripe = wid % VMP_QSTRIPES, dry = 0;
+  // chunks [loc_c, loc_end) of edge loc_e that did not fit into the slot array
+  // are finished by the warp that owns the edge's round-0 item
+  long long loc_e = 0;
+  int loc_c = 0, loc_end = 0, loc_n = 0;
+  for (;;) {{
+{"    const unsigned long long t_top = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
+    long long ei, t = -1;
+    int n, ci, fe = 0;
+    bool round0 = false;
+    if (loc_c < loc_end) {{
+      ei = loc_e;
+      ci = loc_c++;
+      n = loc_n;
+      fe = __ldcg(a.fail + ei);
+    }} else if (r0 < E) {{                     // round 0: edge r0, discretised here
+      ei = t = r0;
+      r0 += nwarps;
+      ci = 0;
+      round0 = true;
+      n = vmp_discretize_edge<{lay.dof}>(a.starts + ei * a.sld, a.goals + ei * a.sld, a.resolution);
+    }} else {{
+      if (tag == 0) {{
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        tag = (1ull + __ldcg(a.dq + VMP_DQ_CALLS) % 65535ull) << 48;
+      }}
+      // the queue is striped over VMP_QSTRIPES pop counters (slot i belongs to
+      // stripe i % VMP_QSTRIPES): thousands of warps leave round 0 within a few
+      // microseconds and same-address atomics serialise in L2
+      long long i;
+      unsigned long long w0, w1, st;
+      for (;;) {{
+        if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
+        i = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
+        have = false;
+        unsigned spins = 0;
+        for (;;) {{
+          ulonglong2 w = make_ulonglong2(0ull, 0ull);
+          if (i < cap) w = __ldcg((const ulonglong2 *)(a.slots + 2 * i));
+          st = __ldcg(state);
+          w0 = w.x;
+          w1 = w.y;
+          if ((w0 >> 48 << 48) == tag && (w1 >> 48 << 48) == tag) break;
+          // not published (yet): more can only come while round 0 is running
+          w0 = 0;
+          if ((long long)(st >> 40) == E && i >= min((long long)(st & M40), cap)) break;
+          if (++spins > (1u << 22)) __trap();   // cannot happen: fail loudly, never hang
+          __nanosleep(40);
+        }}
+        if (w0 != 0) break;
+        // this stripe is dry (round 0 is over, so the slot count is final): any other?
+        const long long total = min((long long)(st & M40), cap);
+        const unsigned long long seen = lane < VMP_QSTRIPES ? __ldcg(&a.hdr->counter[16 * lane]) : 0;
+        const unsigned open = __ballot_sync(VMP_FULL, lane < VMP_QSTRIPES &&
+                                            (long long)seen * VMP_QSTRIPES + lane < total);
+        if (!open || ++dry > 4 * VMP_QSTRIPES) break;
+        stripe = __ffs(open) - 1;
+      }}
+      if (w0 == 0) break;                    // queue drained: this warp is done
+      t = E + i;
+      const long long total = (long long)(st >> 40) == E ? min((long long)(st & M40), cap)
+                                                         : 0x7fffffffffffffffll;
+      if (i + guard < total) {{
+        if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
+        have = true;
+      }}
+      ei = (long long)(w0 & 0x7fffffffull);
+      n = (int)(w1 & 0x7fffffffull);
+      ci = (int)(((w0 >> 31) & 0x1ffffull) | (((w1 >> 31) & 0x3ffull) << 17));
+      fe = __ldcg(a.fail + ei);
+    }}
+    ++taken;
+    const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
+{"    const unsigned long long t_start = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
+    if (fe == 0 || 0x7fffffff - fe > (int)first_iter) {{   // else: cannot lower the count
+      float s[{dofp}], g[{dofp}];
+#pragma unroll
+      for (int j = 0; j < {lay.dof}; ++j) {{
+        s[j] = __ldg(a.starts + ei * a.sld + j);
+        g[j] = __ldg(a.goals + ei * a.sld + j);
+      }}
+      const unsigned S = Wu == 32 ? ((unsigned)n + 31u) >> 5 : vmp_ceil_div((unsigned)n, Wu);
+      const unsigned p = 32u * (unsigned)ci + lane;
+      const unsigned j = Wu == 32 ? (unsigned)ci + 1 : p / Wu + 1;
+      const unsigned k = Wu == 32 ? (unsigned)lane : p - (j - 1) * Wu;
+      const long long idx = (long long)k * S + (a.backward ? (S - j + 1) : j);
+      const bool inr = (unsigned long long)p < (unsigned long long)S * Wu && idx <= n;
+      const float tt = vmp_rake_param(inr ? idx : 1, n);
+      float q[{dofp}];
+#pragma unroll
+      for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
+      bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc, a.env.nb,
+                                                            inr && cclear, 0, 1,
+                                                            STAGED ? &vmp_bar : nullptr);
+      if (!cdone) {{                         // warp-uniform: once, after the first item
+        if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
+        cclear = __all_sync(VMP_FULL, vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, lane, 32));
+        cdone = true;
+        ok = ok && cclear;
+      }}
+      const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
+      if (tag == 0) {{                       // first write to the workspace: begin kernel done?
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        tag = (1ull + __ldcg(a.dq + VMP_DQ_CALLS) % 65535ull) << 48;
+      }}
+      if (bad && lane == 0) {{
+        const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
+        atomicMax(a.fail + ei, 0x7fffffff - (int)it);
+      }}
+      if (round0) {{                         // publish the edge's remaining chunks
+        const int chunks = (int)vmp_rake_chunks((unsigned)n, Wu);
+        // rake positions grow with the chunk index, so no later chunk can fail
+        // at an earlier iteration than one found here: a failed edge is finished
+        const int cnt = bad ? 0 : chunks - 1;
+        unsigned long long base = 0;
+        if (lane == 0) {{
+          a.n_of[ei] = n;
+          base = atomicAdd(state, (1ull << 40) + (unsigned long long)cnt) & M40;
+        }}
+        base = __shfl_sync(VMP_FULL, base, 0);
+        const long long fit = max(0ll, min((long long)cnt, cap - (long long)base));
+        for (long long jx = lane; jx < fit; jx += 32) {{
+          const unsigned long long c = (unsigned long long)(jx + 1);
+          ulonglong2 w;
+          w.x = tag | ((c & 0x1ffffull) << 31) | (unsigned long long)ei;
+          w.y = tag | ((c >> 17) << 31) | (unsigned long long)(unsigned)n;
+          __stcg((ulonglong2 *)(a.slots + 2 * ((long long)base + jx)), w);
+        }}
+        if (fit < cnt) {{
+          loc_e = ei;
+          loc_n = n;
+          loc_c = (int)fit + 1;
+          loc_end = chunks;
+        }}
+      }}
+    }}
+{_TRACE_BLOCK.replace("t < VMP_TRACE_ITEMS", "t >= 0 && t < VMP_TRACE_ITEMS") if TRACE_ITEMS else ""}
+  }}
+  if (trace && lane == 0) {{
+    trace[2 + warp] = vmp_gtime();
+    atomicAdd(trace + 7, (unsigned long long)taken);
+  }}
+  if (STAGED && !cdone) vmp_mbar_wait(&vmp_bar, 0);   // no item evaluated: still retire the copy
   if (trace && threadIdx.x == 0) trace[6] = vmp_gtime();
 }}
 """
@@ -1088,7 +1289,16 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                         f'vmp_motion_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '
                         f'{{ vmp_motion_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
+                        f'vmp_motionq_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '
+                        f'{{ vmp_motion_dq_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
             if staged:
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
+                        f'vmp_motionq_p{prune}_s2_g1_o(VmpMotionArgs a) '
+                        f'{{ vmp_motion_dq_body<{prune}, 2, true>(a); }}\n')
+                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
+                        f'vmp_motionq_p{prune}_s2_g1_o_ns(VmpMotionArgs a) '
+                        f'{{ vmp_motion_dq_body<{prune}, 2, true, true>(a); }}\n')
                 # the hot rake variant, register-capped for MOTION_MIN_CTAS CTAs per
                 # SM; the host uses it only when it compiled without local memory
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '

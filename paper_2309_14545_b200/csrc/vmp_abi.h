@@ -62,6 +62,34 @@ typedef struct {
   unsigned int pad_[2];           /* keep the arrays behind 16-byte aligned */
 } VmpMotionHeader;
 
+/* Dynamic-queue rake (batches up to VMP_DQ_MAX_EDGES edges per launch; the
+ * default).  No plan: round 0 - the first chunk of every edge, discretised by
+ * the item itself - is dealt out statically; an edge whose first iteration
+ * passed publishes its remaining chunks as slot records, which warps then pop.
+ * Only surviving edges ever enter the queue.  Workspace regions used (laid out
+ * by the capacity the workspace size implies):
+ *   hdr->counter[16 s]     pop counter of stripe s: its k-th pop is slot
+ *                          VMP_QSTRIPES k + s (one 128 B line per stripe)
+ *   dq[VMP_DQ_STATE]       (round-0 items finished) << 40 | slots reserved: one
+ *                          atomicAdd per round-0 item both reserves its slots
+ *                          and counts it done, so a reader gets both at once
+ *   dq[VMP_DQ_CALLS]       calls on this workspace; slot tag = 1 + calls % 65535
+ *                          (dq = the 64-bit words behind the header, one line each)
+ *   int fail[E_dq]         per edge: INT_MAX - first failing iteration, 0 = none
+ *   int n[E_dq]            per edge: discretisation count (written by round 0)
+ *   u64 slots[2 * cap]     slot i = two self-validating words
+ *                          w0 = tag << 48 | (chunk & 0x1ffff) << 31 | edge
+ *                          w1 = tag << 48 | (chunk >> 17) << 31 | n
+ *                          (each 8-byte word is written and read whole and
+ *                          carries the call's tag: no fence, no zeroing)
+ * vmp_k_motion_begin (one CTA) resets the counters, zeroes fail[] and bumps the
+ * call count before the rake's first write (programmatic dependent launch). */
+#define VMP_DQ_STATE 0
+#define VMP_DQ_CALLS 16
+#define VMP_DQ_MAX_EDGES (1 << 22)
+#define VMP_DQ_SLOTS_PER_EDGE 8   /* slot capacity per edge of workspace capacity; an edge
+                                     whose chunks do not fit is finished by its own warp */
+
 typedef struct {
   const float *starts; /* (n_edges, sld) float32 AoS */
   const float *goals;  /* (n_edges, sld) float32 AoS */
@@ -85,6 +113,12 @@ typedef struct {
   int guard_waves;      /* stop prefetching queue items this many items per warp
                            before the end (4 for an isolated batch; 1 when batches
                            overlap, whose tails the next batch fills) */
+  /* dynamic-queue rake */
+  int *fail;            /* per edge failure record */
+  int *n_of;            /* per edge discretisation count */
+  unsigned long long *slots; /* 2 words per slot */
+  unsigned long long *dq;    /* state / call-count words */
+  long long slot_cap;   /* slots the workspace holds */
 } VmpMotionArgs;
 
 typedef struct {
