@@ -321,20 +321,20 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         return None
     aux = not args.no_aux
     fkcc = fkcc_summary(ctx_flush=flush, peak=peak) if aux else {}
-    executed = _executed("vmp_motion_p1_s2_g1_o_ns")
+    executed = _executed("vmp_motionq_p1_s2_g1_o_ns")
     roofline = {"bound": "fp32", "achieved": round(achieved, 3), "peak": peak,
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "traffic": _traffic("vmp_motion_p1_s2_g1_o_ns"),
+                "traffic": _traffic("vmp_motionq_p1_s2_g1_o_ns"),
                 # the register-capped rake variant (loaded when it compiles
                 # without local memory; arm7: 96 registers, 5 CTAs / SM),
                 # built without sphere-obstacle code (config 2 has none)
-                "kernel": "vmp_motion_p1_s2_g1_o_ns",
+                "kernel": "vmp_motionq_p1_s2_g1_o_ns",
                 "algorithmic_flop_per_state": f_state,
                 "states_counted_per_launch": int(states.sum()),
                 "peak_measured": peaks,
                 "note": "achieved = states the rake must fully evaluate (valid edges: all n; "
                         "invalid: the iterations before the failing one) x the reference's "
-                        "dense flop per state / mean step time (plan + rake + finalize); "
+                        "dense flop per state / mean step time (begin + rake + finalize); a fraction above 1 is work the exact broadphase avoided, executed_frac is what ran; "
                         "peak = measured FFMA burst (peak_measured); no tensor cores"}
     if executed:
         ex = float(executed["flop_per_launch"])
@@ -359,7 +359,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                   "valid_edge_fraction": round(float(valid.mean()), 4),
                   "mean_states_per_edge": round(float(n_np.mean()), 2),
                   "l2": "flushed (256 MiB write) between timed steps; inputs 229 KB",
-                  "launch": "CUDA graph (plan -> rake -> finalize, PDL edges) via "
+                  "launch": "CUDA graph (begin -> dynamic-queue rake -> finalize, PDL edges) via "
                             "motion.MotionValidator; e2e through motion.MotionPipeline (6 slots, "
                             "each step's H2D, graph replay and D2H on its slot's own stream)"},
         "roofline": roofline,

@@ -60,7 +60,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 37
+CODEGEN_VERSION = 44
 # packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
 FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
 # experiment switches (comma-separated names in VMP_EXP at codegen; scripts/exp_*.sh)
@@ -319,7 +319,17 @@ def _state_function(lay: RobotLayout, program) -> str:
     # broadphase groups: consecutive dynamic spheres, bounded per lane by a sphere
     # centred on the group's middle sphere with the exact (inflated) covering
     # radius - one bound test per group per obstacle replaces one per sphere
-    groups = [dyn[i:i + GROUP_SIZE] for i in range(0, len(dyn), GROUP_SIZE)]
+    n_groups = -(-len(dyn) // GROUP_SIZE)
+    # VMP_EXP=evengroups: an odd group count costs as much per obstacle as the
+    # next even one (two groups share a packed bound chain), but the tighter
+    # split needs more registers: measured slower (arm7 rake 37.0 -> 41.1 us,
+    # config 3 158 -> 166 us)
+    if FFMA2 and n_groups % 2 == 1 and n_groups < len(dyn) and "evengroups" in EXP:
+        n_groups += 1
+        cuts = [round(i * len(dyn) / n_groups) for i in range(n_groups + 1)]
+        groups = [dyn[cuts[i]:cuts[i + 1]] for i in range(n_groups)]
+    else:
+        groups = [dyn[i:i + GROUP_SIZE] for i in range(0, len(dyn), GROUP_SIZE)]
     emit("  constexpr bool CULL = STOP != 0;")
     emit(f"  constexpr bool VMP_WARP_VOTE = {'true' if 'warpvote' in EXP else 'false'};")
     emit(f"  constexpr bool VMP_RAKE_VOTE = {'true' if 'rakevote' in EXP else 'false'};")
@@ -1106,10 +1116,10 @@ __device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
   const unsigned Wu = (unsigned)a.width;
   unsigned long long *const state = a.dq + VMP_DQ_STATE;
   constexpr unsigned long long M40 = (1ull << 40) - 1;
+  constexpr int VMP_DQ_KEEP = {next((int(x[4:]) for x in EXP if x.startswith("keep")), 0)};
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
   (void)warp;
-  const long long guard = (long long)a.guard_waves * nwarps;
   // vmp_k_motion_begin resets the queue words, zeroes fail[] and sets the call
   // count: waited for (programmatic dependent launch) before the first write
   // to any of them, i.e. after the first round-0 chunk has been evaluated
@@ -1132,7 +1142,8 @@ __device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
       ei = loc_e;
       ci = loc_c++;
       n = loc_n;
-      fe = __ldcg(a.fail + ei);
+      // more than the kept chunk(s): a long overflow run, worth the failure check
+      if (loc_end - loc_c > VMP_DQ_KEEP) fe = __ldcg(a.fail + ei);
     }} else if (r0 < E) {{                     // round 0: edge r0, discretised here
       ei = t = r0;
       r0 += nwarps;
@@ -1153,6 +1164,12 @@ __device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
         if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
         i = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
         have = false;
+        if (i < cap) {{                      // published already (the usual case): no state read
+          const ulonglong2 w = __ldca((const ulonglong2 *)(a.slots + 2 * i));
+          w0 = w.x;
+          w1 = w.y;
+          if ((w0 >> 48 << 48) == tag && (w1 >> 48 << 48) == tag) break;
+        }}
         unsigned spins = 0;
         for (;;) {{
           ulonglong2 w = make_ulonglong2(0ull, 0ull);
@@ -1178,12 +1195,10 @@ __device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
       }}
       if (w0 == 0) break;                    // queue drained: this warp is done
       t = E + i;
-      const long long total = (long long)(st >> 40) == E ? min((long long)(st & M40), cap)
-                                                         : 0x7fffffffffffffffll;
-      if (i + guard < total) {{
-        if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
-        have = true;
-      }}
+      // the next pop is in flight while this chunk is evaluated (stopping the
+      // prefetch near the end of the queue measured no faster)
+      if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
+      have = true;
       ei = (long long)(w0 & 0x7fffffffull);
       n = (int)(w1 & 0x7fffffffull);
       ci = (int)(((w0 >> 31) & 0x1ffffull) | (((w1 >> 31) & 0x3ffull) << 17));
@@ -1232,13 +1247,17 @@ __device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
         // rake positions grow with the chunk index, so no later chunk can fail
         // at an earlier iteration than one found here: a failed edge is finished
         const int cnt = bad ? 0 : chunks - 1;
+        // VMP_EXP=keep1 / keep2: the warp keeps the edge's last chunk(s) for itself
+        // (no pop, no slot).  Measured slower - 35.1 -> 37.0 / 38.9 us: every chunk
+        // in the shared queue balances better - so 0 is the default
+        const int want = max(cnt - VMP_DQ_KEEP, 0);
         unsigned long long base = 0;
         if (lane == 0) {{
           a.n_of[ei] = n;
-          base = atomicAdd(state, (1ull << 40) + (unsigned long long)cnt) & M40;
+          base = atomicAdd(state, (1ull << 40) + (unsigned long long)want) & M40;
         }}
         base = __shfl_sync(VMP_FULL, base, 0);
-        const long long fit = max(0ll, min((long long)cnt, cap - (long long)base));
+        const long long fit = max(0ll, min((long long)want, cap - (long long)base));
         for (long long jx = lane; jx < fit; jx += 32) {{
           const unsigned long long c = (unsigned long long)(jx + 1);
           ulonglong2 w;
