@@ -321,14 +321,14 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         return None
     aux = not args.no_aux
     fkcc = fkcc_summary(ctx_flush=flush, peak=peak) if aux else {}
-    executed = _executed("vmp_motionq_p1_s2_g1_o_ns")
+    executed = _executed("vmp_motion_p1_s2_g1_o_ns")
     roofline = {"bound": "fp32", "achieved": round(achieved, 3), "peak": peak,
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "traffic": _traffic("vmp_motionq_p1_s2_g1_o_ns"),
+                "traffic": _traffic("vmp_motion_p1_s2_g1_o_ns"),
                 # the register-capped rake variant (loaded when it compiles
                 # without local memory; arm7: 96 registers, 5 CTAs / SM),
                 # built without sphere-obstacle code (config 2 has none)
-                "kernel": "vmp_motionq_p1_s2_g1_o_ns",
+                "kernel": "vmp_motion_p1_s2_g1_o_ns",
                 "algorithmic_flop_per_state": f_state,
                 "states_counted_per_launch": int(states.sum()),
                 "peak_measured": peaks,

@@ -44,8 +44,8 @@ extern "C" {
                                 batches of resident configurations, ConfigStream)  */
 /* vmp_validate_motions flags (reference motion.py:38-90) */
 #define VMP_BACKWARD 16u     /* comb each stratum top-down (backward=True)            */
-#define VMP_OVERLAPPED 512u  /* batches overlap on several streams (a pipeline):
-                                keep prefetching work items until the queue's end  */
+#define VMP_OVERLAPPED 512u  /* batches overlap on several streams (a pipeline); a
+                                hint, accepted and currently without effect         */
 
 typedef struct vmp_robot vmp_robot; /* compiled module for one KinematicProgram (+pairs) */
 typedef struct vmp_env vmp_env;     /* device-resident packed obstacles                   */
@@ -128,12 +128,14 @@ int vmp_validate(const vmp_robot *robot, const vmp_env *env, const float *q, int
  *   n_states   : optional, discretization_count per edge (motion.py:25-29)
  *   blocks     : optional, block evaluations the W-wide rake performs
  *   workspace  : >= vmp_motion_workspace_bytes(n_edges) bytes of device
- *                scratch (work queue + per-edge plan); 16-byte aligned and
- *                ZERO-FILLED before its first use.  Its layout depends only
- *                on workspace_bytes, so one workspace serves batches of any
- *                size it holds; each call resets the queue counters itself
- *                and re-zeroes its edges' failure records when it finishes
- * Launches plan -> fused FK+CC rake -> finalize on `stream`. */
+ *                scratch (work queue, per-edge failure records and counts);
+ *                16-byte aligned and ZERO-FILLED before its first use.  Its
+ *                layout depends only on workspace_bytes, so one workspace
+ *                serves batches of any size it holds; each call resets the
+ *                queue and the failure records itself before it uses them
+ *                (whatever an earlier call left behind)
+ * Launches begin (reset) -> fused FK+CC rake -> finalize on `stream`, chained
+ * by programmatic dependent launch; above 2^22 edges in sub-batches. */
 int vmp_validate_motions(const vmp_robot *robot, const vmp_env *env, const float *starts,
                          const float *goals, int64_t n_edges, int64_t sld, double resolution,
                          int32_t width, uint32_t flags, uint32_t *valid_bits, int32_t *n_states,

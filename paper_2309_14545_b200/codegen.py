@@ -60,7 +60,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 44
+CODEGEN_VERSION = 46
 # packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
 FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
 # experiment switches (comma-separated names in VMP_EXP at codegen; scripts/exp_*.sh)
@@ -924,172 +924,6 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
 
 template <int PRUNE, int STOP, bool STAGED, bool NO_SPH = false>
 __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
-  // Work items are (chunk c, edge e) pairs enumerated round by round (c-major,
-  // dense).  Chunk c is rake positions [32c, 32c + 32) of the W-lane rake
-  // sequence - exactly one rake iteration when W = 32.  Round 0 holds every
-  // edge, in input order, and needs nothing from the plan: its items compute
-  // their edge's discretisation themselves and run while the plan kernel
-  // (programmatic dependent launch) sorts the edges by chunk count for rounds
-  // >= 1; a warp waits for the plan only when it first reaches round 1.  One
-  // item per atomic keeps the work granularity at one warp-chunk; items of
-  // edges already known to fail at an earlier iteration are skipped.  The
-  // finalize kernel (programmatic dependent launch) writes the outputs.
-  extern __shared__ float4 vmp_smem[];
-  __shared__ unsigned long long vmp_bar;
-  __shared__ long long vmp_off[{BLOCK} / 32][VMP_OFF_CACHE];   // per-warp round offsets
-  // debug timeline (a.trace, VMP_MOTION_TRACE): 8 words per CTA
-  unsigned long long *trace = a.trace ? a.trace + 8 * blockIdx.x : nullptr;
-  if (trace && threadIdx.x == 0) trace[0] = vmp_gtime();
-  // the finalize kernel may launch now: its CTAs fill SM slots as rake CTAs
-  // retire and wait (griddepcontrol.wait) for this whole grid
-  asm volatile("griddepcontrol.launch_dependents;");
-  // the environment copy overlaps the first item's queue atomic, edge loads,
-  // interpolation, FK and self pairs: vmp_state waits for it before the first
-  // obstacle, and each warp checks the constant spheres once, after its first
-  // item (a warp-level vote: no CTA barrier inside the item loop)
-  const float4 *env = a.env.rec;
-  if (STAGED) {{
-    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
-    __syncthreads();                         // the mbarrier is initialised
-    env = vmp_smem;{"""
-    vmp_mbar_wait(&vmp_bar, 0);              // VMP_EXP=waitenv: no overlap (A/B)""" if "waitenv" in EXP else ""}
-  }}
-  bool cclear = true, cdone = false;
-  if (trace && threadIdx.x == 0) trace[1] = vmp_gtime();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long E = a.n_edges;
-  const unsigned Wu = (unsigned)a.width;   // 32-bit rake index math (n < 2^31, positions
-                                           // < 2^31 guarded by the plan)
-  // until the plan is read, only round 0 (items t < E) is known to exist
-  long long total_items = E, split = 0, n_big = 0;
-  int n_off = 0;
-  bool planned = false;
-  unsigned taken = 0;
-  // striped work queue: stripe s serves items t = VMP_QSTRIPES * i + s; a warp
-  // starts on its own stripe and moves on when it runs dry
-  const int wid = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
-  int stripe = wid % VMP_QSTRIPES, dry = 0;
-  // the next item's atomic is issued before the current chunk is evaluated
-  // (hides the L2 atomic round trip) unless the queue is within guard_waves
-  // items per warp of its end, where holding a reserved item lengthens the
-  // tail of an isolated batch (1 / 2 / 4 / 8 items per warp: 47.1 / 46.1 /
-  // 45.05 / 45.1 us); overlapped batches fill each other's tails (1: 38.1 us
-  // per pipelined step, 4: 39.2)
-  const long long guard = (long long)a.guard_waves * gridDim.x * (blockDim.x >> 5);
-  unsigned long long grab = 0;
-  bool have = false;
-  for (;;) {{
-{"    const unsigned long long t_top = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
-    if (!have && lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
-    const long long t = (long long)__shfl_sync(VMP_FULL, grab, 0) * VMP_QSTRIPES + stripe;
-    have = false;
-    if (t >= total_items && !planned) {{     // first item past round 0: read the plan
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      // plan data was written while this grid was already running: read it
-      // through L2 (ld.global.cg), never the non-coherent path
-      total_items = (long long)__ldcg(&a.hdr->total_items);
-      split = __ldcg(a.off + (VMP_HBINS - 1));
-      n_big = __ldcg(&a.hdr->n_big);
-      n_off = (int)min(__ldcg(&a.hdr->max_chunks) + 1u, (unsigned)VMP_HBINS);
-      for (int i = lane; i < min(n_off, VMP_OFF_CACHE); i += 32) vmp_off[warp][i] = __ldcg(a.off + i);
-      __syncwarp();
-      planned = true;
-    }}
-    if (t >= total_items) {{                // stripe dry: look at all stripes at once
-      const unsigned long long seen = lane < VMP_QSTRIPES ? __ldcg(&a.hdr->counter[16 * lane]) : 0;
-      const unsigned open = __ballot_sync(VMP_FULL, lane < VMP_QSTRIPES &&
-                                          (long long)seen * VMP_QSTRIPES + lane < total_items);
-      if (!open || ++dry > 4 * VMP_QSTRIPES) {{
-        if (trace && lane == 0) {{
-          trace[2 + warp] = vmp_gtime();
-          atomicAdd(trace + 7, (unsigned long long)taken);
-        }}
-        break;
-      }}
-      stripe = __ffs(open) - 1;
-      continue;
-    }}
-    ++taken;
-    if (t + guard < total_items) {{
-      if (lane == 0) grab = atomicAdd(&a.hdr->counter[16 * stripe], 1ull);
-      have = true;
-    }}
-    long long ci, ei, ri = -1;
-    int n, chunks, fe = 0;
-    if (t < E) {{                            // round 0: edge t, discretised here; its
-      ci = 0;                               // first iteration can never be skipped
-      ei = t;
-      n = vmp_discretize_edge<{lay.dof}>(a.starts + ei * a.sld, a.goals + ei * a.sld, a.resolution);
-      chunks = (int)vmp_rake_chunks((unsigned)n, Wu);
-    }} else {{
-      if (t < split) {{
-        ci = vmp_find_round_any(vmp_off[warp], a.off, n_off, t, lane);
-        ri = t - (ci < VMP_OFF_CACHE ? vmp_off[warp][ci] : __ldcg(a.off + ci));
-      }} else {{                            // rounds beyond the histogram (very long edges)
-        const long long u = t - split;
-        ci = (VMP_HBINS - 1) + u / n_big;
-        ri = u - (ci - (VMP_HBINS - 1)) * n_big;
-      }}
-      // (edge, n, chunks, failure record): one L2 round trip decides a skip
-      const int4 rank = __ldcg(a.order + ri);
-      ei = rank.x;
-      n = rank.y;
-      chunks = rank.z;
-      fe = rank.w;                          // 0, or INT_MAX - first failing iteration
-    }}
-    if (ci >= chunks) continue;             // absent (only past the histogram)
-    // the native width (W = 32: chunk c is iteration c + 1) skips the divisions
-    const unsigned first_iter = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci) / Wu + 1;
-{"    const unsigned long long t_start = trace ? vmp_gtime() : 0;" if TRACE_ITEMS else ""}
-    if (fe == 0 || 0x7fffffff - fe > (int)first_iter) {{   // else: cannot lower the count
-      float s[{dofp}], g[{dofp}];
-#pragma unroll
-      for (int j = 0; j < {lay.dof}; ++j) {{
-        s[j] = __ldg(a.starts + ei * a.sld + j);
-        g[j] = __ldg(a.goals + ei * a.sld + j);
-      }}
-      const unsigned S = Wu == 32 ? ((unsigned)n + 31u) >> 5 : vmp_ceil_div((unsigned)n, Wu);
-      const unsigned p = 32u * (unsigned)ci + lane;
-      const unsigned j = Wu == 32 ? (unsigned)ci + 1 : p / Wu + 1;
-      const unsigned k = Wu == 32 ? (unsigned)lane : p - (j - 1) * Wu;
-      const long long idx = (long long)k * S + (a.backward ? (S - j + 1) : j);
-      const bool inr = (unsigned long long)p < (unsigned long long)S * Wu && idx <= n;
-      const float tt = vmp_rake_param(inr ? idx : 1, n);
-      float q[{dofp}];
-#pragma unroll
-      for (int jj = 0; jj < {lay.dof}; ++jj) q[jj] = vmp_lerp_exact(s[jj], g[jj], tt);
-      bool ok = vmp_state<STOP, PRUNE != 0, STOP == 2, NO_SPH>(q, env, a.env.ns, a.env.nc, a.env.nb,
-                                                            inr && cclear, 0, 1,
-                                                            STAGED ? &vmp_bar : nullptr);
-      if (!cdone) {{                         // warp-uniform: once, after the first item
-        if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
-        cclear = __all_sync(VMP_FULL, vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb, lane, 32));
-        cdone = true;
-        ok = ok && cclear;
-      }}
-      const unsigned bad = __ballot_sync(VMP_FULL, inr && !ok);
-      if (bad) {{                            // warp-uniform
-        if (ri < 0) {{
-          // a failing round-0 item records into the edge's rank record, which
-          // the plan kernel (usually long finished by now) writes
-          asm volatile("griddepcontrol.wait;" ::: "memory");
-          ri = __ldcg(a.rank_of + ei);
-        }}
-        if (lane == 0) {{
-          const unsigned it = Wu == 32 ? (unsigned)ci + 1 : (32u * (unsigned)ci + __ffs(bad) - 1) / Wu + 1;
-          atomicMax(&a.order[ri].w, 0x7fffffff - (int)it);
-        }}
-      }}
-    }}
-{_TRACE_BLOCK if TRACE_ITEMS else ""}
-
-  }}
-  if (STAGED && !cdone) vmp_mbar_wait(&vmp_bar, 0);   // no item evaluated: still retire the copy
-  if (trace && threadIdx.x == 0) trace[6] = vmp_gtime();
-}}
-
-template <int PRUNE, int STOP, bool STAGED, bool NO_SPH = false>
-__device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
   // Dynamic-queue rake (csrc/vmp_abi.h).  Round 0 - the first chunk of every
   // edge, discretised by the item itself - is dealt out statically (warp w
   // takes edges w, w + warps, ...): no atomics, nothing to wait for.  An edge
@@ -1308,16 +1142,7 @@ __device__ __forceinline__ void vmp_motion_dq_body(const VmpMotionArgs &a) {{
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
                         f'vmp_motion_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '
                         f'{{ vmp_motion_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
-                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}) '
-                        f'vmp_motionq_p{prune}_s{stop}_g{staged}(VmpMotionArgs a) '
-                        f'{{ vmp_motion_dq_body<{prune}, {stop}, {"true" if staged else "false"}>(a); }}\n')
             if staged:
-                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
-                        f'vmp_motionq_p{prune}_s2_g1_o(VmpMotionArgs a) '
-                        f'{{ vmp_motion_dq_body<{prune}, 2, true>(a); }}\n')
-                src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '
-                        f'vmp_motionq_p{prune}_s2_g1_o_ns(VmpMotionArgs a) '
-                        f'{{ vmp_motion_dq_body<{prune}, 2, true, true>(a); }}\n')
                 # the hot rake variant, register-capped for MOTION_MIN_CTAS CTAs per
                 # SM; the host uses it only when it compiled without local memory
                 src += (f'extern "C" __global__ void __launch_bounds__({BLOCK}, {MOTION_MIN_CTAS}) '

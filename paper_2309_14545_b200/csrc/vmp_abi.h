@@ -30,40 +30,8 @@ typedef struct {
   int pad_;
 } VmpValidateArgs;
 
-/* Motion workspace (the per-edge arrays are laid out by the capacity the
- * workspace size implies, E_cap; every call resets the queue counters before
- * the rake starts and rewrites every per-edge record it reads):
- *   VmpMotionHeader
- *   unsigned hist[VMP_HBINS], fill[VMP_HBINS]   chunk-count histogram / scatter cursors
- *   long long off[VMP_HBINS]                    first work item of chunk round c
- *   int rank_of[E_cap]                          per edge: index of its rank record
- *   int n[E_cap], chunks[E_cap]                 per edge: discretisation count and
- *                                               chunks (multi-kernel plan only)
- *   int4 order[E_cap]                           rank records (edge, n, chunks, failure
- *                                               record) by chunk count descending; the
- *                                               failure record is INT_MAX - first failing
- *                                               iteration, 0 while none (atomicMax)
- * Work item t < E is round 0 of edge t (input order, no plan needed); item
- * E <= t < off[HBINS-1] is (round c, rank r): edge order[r], chunk c, where
- * off[c] <= t < off[c+1]; rounds >= HBINS-1 enumerate the n_big longest edges
- * (chunks >= HBINS-1) and skip absent chunks. */
-#define VMP_HBINS 1024
-#define VMP_QSTRIPES 16           /* item queue striped over 16 counters (t % 16) */
-#define VMP_TRACE_ITEM0 8192      /* debug timeline: per-item records start here */
-#define VMP_TRACE_ITEMS 30000     /* items recorded (4 words each) */
-#define VMP_OFF_CACHE 64          /* round offsets a rake warp keeps in shared memory */
-typedef struct {
-  unsigned long long counter[VMP_QSTRIPES * 16]; /* stripe s at [16 s]: one 128 B line each */
-  unsigned long long total_items; /* written by the scan kernel */
-  unsigned int max_chunks;        /* max over edges of ceil(S W / 32), S = ceil(n / W) */
-  unsigned int n_big;             /* edges with chunks >= VMP_HBINS - 1 */
-  unsigned int done_ctas;         /* CTAs of the rake kernel that finished */
-  unsigned int plan_done;         /* reserved (kept zero) */
-  unsigned int pad_[2];           /* keep the arrays behind 16-byte aligned */
-} VmpMotionHeader;
-
-/* Dynamic-queue rake (batches up to VMP_DQ_MAX_EDGES edges per launch; the
- * default).  No plan: round 0 - the first chunk of every edge, discretised by
+/* Motion workspace of the dynamic-queue rake (batches up to VMP_DQ_MAX_EDGES
+ * edges per launch).  No plan: round 0 - the first chunk of every edge, discretised by
  * the item itself - is dealt out statically; an edge whose first iteration
  * passed publishes its remaining chunks as slot records, which warps then pop.
  * Only surviving edges ever enter the queue.  Workspace regions used (laid out
@@ -84,11 +52,18 @@ typedef struct {
  *                          carries the call's tag: no fence, no zeroing)
  * vmp_k_motion_begin (one CTA) resets the counters, zeroes fail[] and bumps the
  * call count before the rake's first write (programmatic dependent launch). */
+#define VMP_QSTRIPES 16           /* slot queue striped over 16 pop counters (slot % 16) */
 #define VMP_DQ_STATE 0
 #define VMP_DQ_CALLS 16
 #define VMP_DQ_MAX_EDGES (1 << 22)
-#define VMP_DQ_SLOTS_PER_EDGE 8   /* slot capacity per edge of workspace capacity; an edge
-                                     whose chunks do not fit is finished by its own warp */
+#define VMP_DQ_SLOTS_PER_EDGE 8   /* slot capacity per edge of workspace capacity (plus a
+                                     fixed spare); an edge whose chunks do not fit is
+                                     finished by its own warp */
+#define VMP_TRACE_ITEM0 8192      /* debug timeline: per-item records start here */
+#define VMP_TRACE_ITEMS 30000     /* items recorded (4 words each) */
+typedef struct {
+  unsigned long long counter[VMP_QSTRIPES * 16]; /* stripe s at [16 s]: one 128 B line each */
+} VmpMotionHeader;
 
 typedef struct {
   const float *starts; /* (n_edges, sld) float32 AoS */
@@ -98,22 +73,13 @@ typedef struct {
   double resolution;
   VmpEnvView env;
   VmpMotionHeader *hdr;
-  const long long *off; /* first work item of each chunk round */
-  int4 *order;          /* rank records (edge, n, chunks, failure record), chunk count
-                           descending; .w = INT_MAX - first failing iteration, 0 while none */
-  const int *rank_of;   /* per edge: index of its rank record (read by failing round-0
-                           items after the plan, and by finalize) */
-  int *pad_ptr_;        /* reserved */
   unsigned long long *trace; /* debug timeline (VMP_MOTION_TRACE), normally null:
-                                per CTA [entry, plan ready, warp 0-3 queue empty,
+                                per CTA [entry, first wait over, warp 0-3 queue empty,
                                 exit, work items taken] in globaltimer ns */
   int width;            /* rake lane width W whose block counts are reproduced */
   int backward;         /* comb strata top-down */
   int stage;
-  int guard_waves;      /* stop prefetching queue items this many items per warp
-                           before the end (4 for an isolated batch; 1 when batches
-                           overlap, whose tails the next batch fills) */
-  /* dynamic-queue rake */
+  int pad_;
   int *fail;            /* per edge failure record */
   int *n_of;            /* per edge discretisation count */
   unsigned long long *slots; /* 2 words per slot */

@@ -468,33 +468,6 @@ __device__ __forceinline__ float vmp_lerp_exact(float s, float g, float t) {
   return __fadd_rn(s, __fmul_rn(t, __fsub_rn(g, s)));
 }
 
-/* Outputs of edges [tid0 + tid, ...) stepping by nthreads (whole warps):
- * verdict word by ballot, n and the W-lane rake block count.  An edge's
- * outcome lives in its rank record (edge, n, chunks, failure record) at
- * order[rank_of[edge]]; the failure record is INT_MAX - first failing
- * iteration, 0 = none (the plan rewrites every record each call). */
-__device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w);
-__device__ __forceinline__ void vmp_motion_outputs(long long n_edges, int width, const int *rank_of,
-                                                   const int4 *order, unsigned *bits, int *n_states,
-                                                   int *blocks, long long tid0, long long nthreads,
-                                                   int tid) {
-  for (long long base = tid0; base < n_edges; base += nthreads) {
-    const long long e = base + tid;
-    const bool inr = e < n_edges;
-    int4 rec = make_int4(0, 0, 0, 1);
-    if (inr) rec = __ldcg(order + __ldcg(rank_of + e));
-    const int fe = rec.w;
-    const bool ok = inr && fe == 0;
-    const unsigned m = __ballot_sync(VMP_FULL, ok);
-    if (inr) {
-      if ((tid & 31) == 0) bits[e >> 5] = m;
-      const int n = rec.y;
-      if (n_states) n_states[e] = n;
-      if (blocks) blocks[e] = ok ? (int)vmp_ceil_div((unsigned)n, (unsigned)width) : 0x7fffffff - fe;
-    }
-  }
-}
-
 /* ceil(n / w) and the number of 32-position chunks of a W-lane rake over n
  * states, with 32-bit division (n < 2^31, w >= 1). */
 __device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w) {
@@ -502,36 +475,6 @@ __device__ __forceinline__ unsigned vmp_ceil_div(unsigned n, unsigned w) {
 }
 __device__ __forceinline__ unsigned vmp_rake_chunks(unsigned n, unsigned w) {
   return (unsigned)(((unsigned long long)vmp_ceil_div(n, w) * w + 31ull) >> 5);
-}
-
-
-
-/* Same, with the first VMP_OFF_CACHE offsets in shared memory and the rest
- * read through L2. */
-__device__ __forceinline__ int vmp_find_round_any(const long long *off_s, const long long *off_g,
-                                                  int n_off, long long t, int lane) {
-  int base = 0;
-  for (;;) {
-    const int c = base + lane;
-    const bool le = c < n_off && (c < VMP_OFF_CACHE ? off_s[c] : __ldcg(off_g + c)) <= t;
-    const unsigned m = __ballot_sync(VMP_FULL, le);
-    if (m != VMP_FULL || base + 32 >= VMP_HBINS) return base + 31 - __clz(m);
-    base += 32;
-  }
-}
-
-/* Round c of the motion work list holding item t: the largest c with
- * off[c] <= t, found 32 rounds per step with one load per lane + ballot. */
-__device__ __forceinline__ int vmp_find_round(const long long *off, int n_off, long long t,
-                                              int lane) {
-  int base = 0;
-  for (;;) {
-    const int c = base + lane;
-    const bool le = c < n_off && off[c] <= t;
-    const unsigned m = __ballot_sync(VMP_FULL, le);
-    if (m != VMP_FULL || base + 32 >= VMP_HBINS) return base + 31 - __clz(m);
-    base += 32;
-  }
 }
 
 #endif

@@ -71,7 +71,7 @@ def raked_motion_check(start: Config, goal: Config, ctx: ValidationContext,
     if s.shape[0] != ctx.program.dof:
         raise ValueError(f"block dim {s.shape[0]} != program dof {ctx.program.dof}")
     ctx.motion_checks += 1
-    # one host-buffer C call: pinned staging -> plan + rake + finalize -> read-back
+    # one host-buffer C call: pinned staging -> begin + rake + finalize -> read-back
     verdict, _, blocks = runtime.motions_host(*_bind(ctx), s.reshape(1, -1), g.reshape(1, -1),
                                               resolution, width=ctx.width, backward=backward,
                                               prune=getattr(ctx, "prune", True))
@@ -91,7 +91,7 @@ class MotionValidator:
     """Fixed-size batched rake with device-resident buffers and a CUDA graph.
 
     For callers that validate many batches of ``n_edges`` edges (planner
-    rounds, the benchmark): the plan and rake launches are captured once and
+    rounds, the benchmark): the begin, rake and finalize launches are captured once and
     replayed, so a call costs one graph launch.  ``__call__`` copies the edges
     into the resident buffers (from host memory - pinned for async copies - or
     from device tensors), replays, and returns the packed int32 verdict words
@@ -156,7 +156,7 @@ class MotionPipeline:
 
     Each slot (a ``MotionValidator``: device buffers + CUDA graph) owns a
     stream, and ``submit(starts, goals)`` enqueues the whole step on it: the
-    host->device copy of the batch, the graph replay (plan -> rake ->
+    host->device copy of the batch, the graph replay (begin -> rake ->
     finalize) and the verdict read-back into the slot's pinned host buffer.
     Batches in different slots share no stream and no event, so batch k+1's
     copy and rake start while batch k's rake drains (measured: 41.6 us per

@@ -21,7 +21,7 @@ cap() {  # cap <name> <kernel regex> <profile_kernels args...>
   ncu -i gpurun_out/prof_$name.ncu-rep --page raw --csv > gpurun_out/raw_$name.csv 2>/dev/null
   python scripts/executed_flops.py gpurun_out/prof_$name.ncu-rep > gpurun_out/exec_$name.json 2>/dev/null
 }
-cap motion "vmp_motionq?_p" motion
+cap motion "vmp_motion_p" motion
 cap begin "motion_begin" motion
 cap finalize "motion_finalize" motion
 cap cfg1 "vmp_validate" cfg1

@@ -12,5 +12,5 @@ for name in ("arm7", "fetch_standin", "baxter_standin"):
     out = f"/tmp/{name}_nvrtc.cubin"
     check(lib().vmp_compile(src.encode(), f"{name}.cu".encode(), out.encode()))
     ru = subprocess.run(["cuobjdump", "--dump-resource-usage", out], capture_output=True, text=True).stdout
-    for m in re.finditer(r"Function (vmp_motionq?_p1_s2_g1\w*|vmp_validate_p1_s1_g1)\b.*?\n.*?REG:(\d+) STACK:(\d+)", ru):
+    for m in re.finditer(r"Function (vmp_motion_p1_s2_g1\w*|vmp_validate_p1_s1_g1)\b.*?\n.*?REG:(\d+) STACK:(\d+)", ru):
         print(name, m.group(1), "REG", m.group(2), "STACK", m.group(3))

@@ -381,7 +381,7 @@ def test_motion_errors(cuda):
 
 def test_motion_repeated_calls_consistent(cuda):
     """Back-to-back launches (fresh and reused self-cleaning workspaces, PDL
-    overlap of plan and rake kernels) give identical results every time."""
+    overlap of the begin, rake and finalize kernels) give identical results every time."""
     fx = golden_io.load("motion")
     key = "arm7_0"
     rob = load_robot("arm7")
@@ -403,9 +403,9 @@ def test_motion_repeated_calls_consistent(cuda):
 
 
 @pytest.mark.parametrize("tiles", [1, 3, 17])   # 4,096 / 12,288 / 69,632 edges
-def test_motion_plan_paths_agree(cuda, tiles):
-    """The three plan paths (one edge per cluster thread up to 8,192 edges,
-    eight per thread up to 65,536, multi-kernel plan above) give the verdicts,
+def test_motion_batch_sizes_agree(cuda, tiles):
+    """Batches of 1 / 3 / 17 copies of the config-2 edges (round 0 of one wave,
+    of several waves per warp, and a queue far longer than the grid) give the verdicts,
     n and W-block counts of the oracle-checked 4,096-edge config 2 batch."""
     mw = workloads.config2()
     rob = load_robot("arm7")
@@ -425,10 +425,11 @@ def test_motion_plan_paths_agree(cuda, tiles):
 
 
 def test_motion_very_long_edges_and_tiny_batches(cuda):
-    """Edges whose chunk count passes the 1,023-round histogram (n up to ~1e5
-    states: the rounds enumerated past `split`), mixed with short edges, a
-    zero-length edge, and batches of 0 / 1 edges - verdicts, n and W-lane
-    block counts equal the dense oracle's."""
+    """Very long edges (n up to ~57,000 states, ~1,800 chunks each) mixed with
+    short ones, a zero-length edge, and batches of 0 / 1 edges - verdicts, n
+    and W-lane block counts equal the dense oracle's.  Then six edges at
+    1/65,536 rad: more chunks than the workspace has slots, so the owning warps
+    finish the chunks that do not fit (the queue's overflow path)."""
     mw = workloads.config2()
     rob = load_robot("arm7")
     ob = O.Obstacles(mw.env.primitives)
@@ -439,7 +440,7 @@ def test_motion_very_long_edges_and_tiny_batches(cuda):
     g[3] = s[3]                                          # zero length: n = 1
     res = 1.0 / 8192.0                                   # n up to ~57,000 states
     ns = [O.discretization(a, b, res) for a, b in zip(s, g)]
-    assert max(ns) > 32 * 1023, "need edges past the chunk histogram"
+    assert max(ns) > 32 * 1023
     states = [O.edge_all_states(rob.program, rob.pairs, ob, a, b, res)[1] for a, b in zip(s, g)]
     for width in (32, 8):
         ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env, width=width)
@@ -454,6 +455,19 @@ def test_motion_very_long_edges_and_tiny_batches(cuda):
     assert empty.numel() == 0
     one = M.validate_motions(ctx, s[:1], g[:1], res)
     assert bool(runtime.unpack_bits(one.cpu().numpy(), 1)[0]) == bool(states[0].all())
+    # overflow: valid edges first, so their chunks are what the queue cannot hold
+    order = np.argsort([not v.all() for v in states], kind="stable")[:6]
+    s6, g6, fine = s[order], g[order], 1.0 / 65536.0
+    n6 = [O.discretization(a, b, fine) for a, b in zip(s6, g6)]
+    chunks = sum((n + 31) // 32 - 1 for n in n6)
+    assert chunks > 8 * 8 + 32768, "need more chunks than slots (csrc/vmp.cu kDqSpareSlots)"
+    st6 = [O.edge_all_states(rob.program, rob.pairs, ob, a, b, fine)[1] for a, b in zip(s6, g6)]
+    bits, n, blk = M.validate_motions(ctx, s6, g6, fine, counts=True)
+    assert n.cpu().numpy().tolist() == n6
+    for i, v in enumerate(st6):
+        ok, blocks = O.rake_blocks_from_states(v, 32)
+        assert bool(runtime.unpack_bits(bits.cpu().numpy(), 6)[i]) == ok, i
+        assert int(blk.cpu().numpy()[i]) == blocks, i
 
 
 @pytest.mark.parametrize("cfg", ["cfg3", "cfg4", "cfg5_16"])
