@@ -228,7 +228,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     rob = load_robot(mw.robot)
     ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
     E = len(mw.starts)
-    # the public fixed-size API: resident edge buffers + CUDA graph of plan + rake
+    # the public fixed-size API: resident edge buffers + CUDA graph of begin + rake
     mv = M.MotionValidator(ctx, E, mw.resolution, width=32)
     mv(mw.starts, mw.goals)
     torch.cuda.synchronize()
@@ -363,7 +363,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
                             "motion.MotionValidator; e2e through motion.MotionPipeline (6 slots, "
                             "each step's H2D, graph replay and D2H on its slot's own stream)"},
         "roofline": roofline,
-        # per step (one graph replay): cluster plan + rake + finalize kernels
+        # per step (one graph replay): begin + rake + finalize kernels
         "gpu_launches": 3 * args.steps,
         "e2e": {"value": round(e2e_value, 1), "unit": "edges/s",
                 "h2d_bytes_per_step": int(mw.starts.nbytes + mw.goals.nbytes),
@@ -520,7 +520,7 @@ def latency_summary(mw, rob, calls: int = 300) -> dict:
             lambda i: M.raked_motion_check(mw.starts[i % 4096], mw.goals[i % 4096], ctx,
                                            mw.resolution), calls),
         "note": "ValidationContext(width=8); raked_motion_check averaged over the first "
-                f"{calls} config-2 edges (plan + rake + finalize per call)",
+                f"{calls} config-2 edges (begin + rake + finalize per call)",
     }
 
 
