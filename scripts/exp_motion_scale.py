@@ -1,5 +1,5 @@
 """Motion rake throughput vs batch size: config-2 edges tiled to 4K .. 1M edges
-(cluster plan <1> / <8> and the multi-kernel plan), L2 flushed per launch."""
+(round 0 of one to hundreds of waves per warp), L2 flushed per launch."""
 import sys
 from pathlib import Path
 
