@@ -167,6 +167,7 @@ def _executed(kernel: str):
 
 
 PARITY = ROOT / "tests" / "golden" / "bench_parity.npz"
+E2E_REPS = 5
 
 
 def _bits(words, n: int) -> np.ndarray:
@@ -288,23 +289,29 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     pipe = M.MotionPipeline(ctx, E, mw.resolution, width=32, depth=depth)
     for _ in range(args.warmup):
         pipe.result(pipe.submit(hs, hg))
-    torch.cuda.synchronize()
-    flush.zero_()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for st in pipe.streams:
-        st.wait_event(a)
-    inflight = []
-    for i in range(args.steps):
-        inflight.append(pipe.submit(hs, hg))
-        if len(inflight) == depth:                        # oldest step's verdicts on the host
-            got = pipe.result(inflight.pop(0))
-    for t in inflight:
-        got = pipe.result(t)
-    pipe.wait_all(stream)
-    b.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = a.elapsed_time(b)
+    # the K-step region lasts under a millisecond, so one host hiccup moves it by
+    # tens of percent: it is timed E2E_REPS times, each from an empty pipeline to
+    # an empty one, and the median is reported (every repetition is in e2e.runs)
+    e2e_runs = []
+    for _ in range(E2E_REPS):
+        torch.cuda.synchronize()
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for st in pipe.streams:
+            st.wait_event(a)
+        inflight = []
+        for i in range(args.steps):
+            inflight.append(pipe.submit(hs, hg))
+            if len(inflight) == depth:                    # oldest step's verdicts on the host
+                got = pipe.result(inflight.pop(0))
+        for t in inflight:
+            got = pipe.result(t)
+        pipe.wait_all(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_runs.append(a.elapsed_time(b))
+    e2e_ms = float(np.median(e2e_runs))
     if world > 1:
         tt = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -366,6 +373,8 @@ def run_ours(args, rank: int, world: int) -> dict | None:
         # per step (one graph replay): begin + rake + finalize kernels
         "gpu_launches": 3 * args.steps,
         "e2e": {"value": round(e2e_value, 1), "unit": "edges/s",
+                "runs_ms": [round(x, 4) for x in e2e_runs],
+                "note": f"median of {E2E_REPS} repetitions of the {args.steps}-step region",
                 "h2d_bytes_per_step": int(mw.starts.nbytes + mw.goals.nbytes),
                 "d2h_bytes_per_step": int(bits.numel() * 4)},
         "clocks": clocks.summary(),

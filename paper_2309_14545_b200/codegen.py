@@ -60,7 +60,7 @@ def fk_tiling(n_rows: int) -> tuple[int, int]:
         if tile_bytes <= FK_SMEM_TILE:
             return per, (2 if 2 * tile_bytes <= 80 * 1024 else 1)
     return 1, 0
-CODEGEN_VERSION = 46
+CODEGEN_VERSION = 49
 # packed FFMA2 (fma.rn.f32x2) broadphase chains; VMP_NO_FFMA2=1 at codegen: scalar
 FFMA2 = __import__("os").environ.get("VMP_NO_FFMA2", "") != "1"
 # experiment switches (comma-separated names in VMP_EXP at codegen; scripts/exp_*.sh)
@@ -282,7 +282,10 @@ def _state_function(lay: RobotLayout, program) -> str:
     emit("__device__ __forceinline__ bool vmp_state(const float *q, const float4 *__restrict__ env,")
     emit("                                          int ns, int nc, int nb, bool ok,")
     emit("                                          int sub = 0, int split = 1,")
-    emit("                                          unsigned long long *bar = nullptr) {")
+    emit("                                          unsigned long long *bar = nullptr,")
+    emit("                                          bool pairs_rt = true) {")
+    emit("  // pairs_rt: the bound-pair records lie behind the obstacle records at env")
+    emit("  (void)pairs_rt;")
     emit("  // split > 1: this thread handles obstacles k = sub (mod split) and self")
     emit("  // pairs i = sub (mod split) of its configuration (small-batch kernels)")
     emit("  (void)env; (void)ns; (void)nc; (void)nb;")
@@ -479,6 +482,30 @@ def _state_function(lay: RobotLayout, program) -> str:
                 emit(ind + f"n{gi} = vmp_push_sign(n{gi}, "
                      f"vmp_near1({mx}, {my}, {mz}, G{gi}S, G{gi}M, bnd, brad));")
 
+    def bound_masks_pair(ind: str) -> None:
+        """Per TWO obstacles (one bound-pair record: bx2, by2, bz2, bw2, br2): the
+        odd group takes both bounds in one packed chain; obstacle 2p + 1 is
+        pushed first so that bit j of a mask stays obstacle j of the chunk."""
+        paired = set()
+        for _, gi in pairs:
+            for half in ("hi", "lo"):
+                emit(ind + f"{{ const vmp_f2 w = vmp_near2s(Q{gi}X, Q{gi}Y, Q{gi}Z, Q{gi}S, Q{gi}M, "
+                     f"vmp_{half}(bx2), vmp_{half}(by2), vmp_{half}(bz2), vmp_{half}(bw2), vmp_{half}(br2)); "
+                     f"n{gi} = vmp_push_sign(n{gi}, vmp_lo(w)); "
+                     f"n{gi + 1} = vmp_push_sign(n{gi + 1}, vmp_hi(w)); }}")
+            paired.update((gi, gi + 1))
+        for gi, grp in enumerate(groups):
+            if gi not in paired:
+                mx, my, mz = _exyz(grp[len(grp) // 2])
+                emit(ind + f"{{ const vmp_f2 w = vmp_near1x2({mx}, {my}, {mz}, G{gi}S, G{gi}M, "
+                     f"bx2, by2, bz2, bw2, br2); "
+                     f"n{gi} = vmp_push_sign(vmp_push_sign(n{gi}, vmp_hi(w)), vmp_lo(w)); }}")
+
+    # the rake tests two obstacle bounds per packed chain for the odd group
+    # (bound-pair records, csrc/vmp_abi.h VMP_PAIR_F4): 26 instead of 34
+    # instructions per two obstacles on arm7
+    use_pairs = FFMA2 and len(groups) % 2 == 1 and "nopairs" not in EXP
+
     def bound_terms() -> list[str]:
         """Per obstacle: the expanded bound distance of every group, as terms
         whose minimum decides "near" (packed pairs first)."""
@@ -613,7 +640,7 @@ def _state_function(lay: RobotLayout, program) -> str:
         return f"{box_fn(r)}({x}, {y}, {z}, {f32_literal(rs2)}, r0, r1, r2, r3)"
 
     def kind_loop(count: str, f4: str, base: str, loads: str, bound: str, radius: str, test_fn,
-                  coarse_fn):
+                  coarse_fn, pair_base: str = ""):
         # dense mode (STOP 0): every obstacle, every test - the honest roofline run
         emit(f"  p = {base} + sub * {f4};")
         emit("  if constexpr (!CULL) {")
@@ -635,6 +662,21 @@ def _state_function(lay: RobotLayout, program) -> str:
         emit(f"    for (int k0 = sub; k0 < {count}; k0 += 32 * split, p += 32 * split * {f4}) {{")
         emit(f"      const int kn = min(32, ({count} - k0 + split - 1) / split);")
         emit("      unsigned " + ", ".join(f"n{gi} = 0" for gi in range(len(groups))) + ";")
+        if use_pairs:
+            # rake / unsplit batch kernels with staged pairs: the chunk's bound pairs, last first
+            emit("      if ((TWO || split == 1) && pairs_rt) {")
+            emit("        const int np = (kn + 1) >> 1;")
+            emit(f"        const ulonglong2 *pq = (const ulonglong2 *)({pair_base}) + "
+                 f"VMP_PAIR_F4 * ((k0 >> 1) + np - 1);")
+            emit("#pragma unroll 1")
+            emit("        for (int j = np - 1; j >= 0; --j, pq -= VMP_PAIR_F4) {")
+            emit("          const ulonglong2 q0 = pq[0], q1 = pq[1];")
+            emit("          const vmp_f2 bx2 = q0.x, by2 = q0.y, bz2 = q1.x, bw2 = q1.y, "
+                 "br2 = *(const vmp_f2 *)(pq + 2);")
+            bound_masks_pair("          ")
+            emit("        }")
+            emit("        // an odd chunk: the pad bound was pushed as obstacle kn, never near")
+            emit("      } else {")
         emit(f"      const float4 *pp = p + (kn - 1) * split * {f4};")
         emit("#pragma unroll 2")
         emit(f"      for (int j = kn - 1; j >= 0; --j, pp -= split * {f4}) {{")
@@ -642,6 +684,8 @@ def _state_function(lay: RobotLayout, program) -> str:
         emit(f"        const float brad = {radius};")
         bound_masks("        ")
         emit("      }")
+        if use_pairs:
+            emit("      }")
         for gi, grp in enumerate(groups):
             emit(f"      while (n{gi} != 0 && ok) {{")
             emit(f"        const int j = __ffs(n{gi}) - 1;")
@@ -712,14 +756,17 @@ def _state_function(lay: RobotLayout, program) -> str:
         # NO_SPH: the rake variant for scenes without sphere obstacles carries no
         # sphere code (a smaller hot loop for the instruction cache)
         emit("  if constexpr (!NO_SPH) {")
+        pairs0 = "(env + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc + VMP_BOX_F4 * nb)"
         kind_loop("ns", "VMP_SPH_F4", "env", "r0 = p[0], r1 = p[1]", "0", "pp[1].x",
-                  sph_test, sph_coarse)
+                  sph_test, sph_coarse, pairs0)
         emit("  }")
         kind_loop("nc", "VMP_CAP_F4", "(env + VMP_SPH_F4 * ns)", "r0 = p[0], r1 = p[1], r2 = p[2]",
-                  "3", "pp[2].w", cap_test, cap_coarse)
+                  "3", "pp[2].w", cap_test, cap_coarse,
+                  f"({pairs0} + VMP_PAIR_F4 * ((ns + 1) >> 1))")
         kind_loop("nb", "VMP_BOX_F4", "(env + VMP_SPH_F4 * ns + VMP_CAP_F4 * nc)",
                   "r0 = p[0], r1 = p[1], r2 = p[2], r3 = p[3]", "4", "pp[3].w",
-                  box_test, box_coarse)
+                  box_test, box_coarse,
+                  f"({pairs0} + VMP_PAIR_F4 * (((ns + 1) >> 1) + ((nc + 1) >> 1)))")
     emit("#undef VMP_STOP_NOW")
     emit("  return ok;")
     emit("}")
@@ -881,8 +928,9 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
   // the environment copy overlaps the joint loads, FK and self pairs of the
   // first tile; vmp_state waits for it before the first obstacle
   const float4 *env = STAGED ? vmp_smem : a.env.rec;
+  const bool vpairs = STAGED && a.stage == 2;   // bound pairs staged behind the records
   if (STAGED) {{
-    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
+    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar, vpairs);
     __syncthreads();
   }}
   bool cclear = true, cdone = false;
@@ -896,7 +944,7 @@ __device__ __forceinline__ void vmp_validate_body(const VmpValidateArgs &a) {{
     float q[{dofp}];
 {ld_q}
     bool ok = vmp_state<STOP, PRUNE != 0, TWO>(q, env, a.env.ns, a.env.nc, a.env.nb, inr, sub,
-                                               SPLIT, STAGED ? &vmp_bar : nullptr);
+                                               SPLIT, STAGED ? &vmp_bar : nullptr, vpairs);
     if (!cdone) {{                            // CTA-uniform: once, after the first tile
       if (STAGED) vmp_mbar_wait(&vmp_bar, 0);
       cclear = __syncthreads_and(vmp_const_clear(env, a.env.ns, a.env.nc, a.env.nb,
@@ -940,7 +988,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
   asm volatile("griddepcontrol.launch_dependents;");
   const float4 *env = a.env.rec;
   if (STAGED) {{
-    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar);
+    vmp_env_begin(a.env, 1, vmp_smem, &vmp_bar, true);   // obstacle records + bound pairs
     __syncthreads();                         // the mbarrier is initialised
     env = vmp_smem;
   }}
@@ -1005,6 +1053,7 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
           if ((w0 >> 48 << 48) == tag && (w1 >> 48 << 48) == tag) break;
         }}
         unsigned spins = 0;
+        unsigned long long spin_t0 = 0;
         for (;;) {{
           ulonglong2 w = make_ulonglong2(0ull, 0ull);
           if (i < cap) w = __ldcg((const ulonglong2 *)(a.slots + 2 * i));
@@ -1015,7 +1064,12 @@ __device__ __forceinline__ void vmp_motion_body(const VmpMotionArgs &a) {{
           // not published (yet): more can only come while round 0 is running
           w0 = 0;
           if ((long long)(st >> 40) == E && i >= min((long long)(st & M40), cap)) break;
-          if (++spins > (1u << 22)) __trap();   // cannot happen: fail loudly, never hang
+          // cannot happen (every reserved slot is written by a running warp): fail
+          // loudly after 20 s rather than hang the device
+          if ((++spins & 1023u) == 0u) {{
+            if (spin_t0 == 0) spin_t0 = vmp_gtime();
+            else if (vmp_gtime() - spin_t0 > 20000000000ull) __trap();
+          }}
           __nanosleep(40);
         }}
         if (w0 != 0) break;

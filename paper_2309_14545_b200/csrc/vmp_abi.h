@@ -11,13 +11,17 @@
 #define VMP_SPH_F4 2
 #define VMP_CAP_F4 4
 #define VMP_BOX_F4 5
+#define VMP_PAIR_F4 3  /* behind the obstacle records, per kind: one record per two
+                          obstacles with their bounding spheres interleaved as
+                          packed operands (xa, xb, ya, yb) (za, zb, wa, wb)
+                          (ra, rb, 0, 0); ceil(n / 2) records per kind */
 typedef struct {
   const float4 *rec;   /* device pointer, 16-byte aligned */
   int ns, nc, nb;      /* sphere / capsule / cuboid counts */
-  int n_f4;            /* total float4 records = 2 ns + 4 nc + 5 nb */
+  int n_f4;            /* per-obstacle float4 records = 2 ns + 4 nc + 5 nb */
   float ox, oy, oz;    /* origin of the environment frame: records hold obstacle
                           geometry minus it, kernels subtract it from sphere centres */
-  int pad_;
+  int n_all_f4;        /* n_f4 + the bound pairs: 3 (ceil(ns / 2) + ceil(nc / 2) + ceil(nb / 2)) */
 } VmpEnvView;
 
 typedef struct {
@@ -26,7 +30,8 @@ typedef struct {
   long long ld;        /* leading dimension of q */
   VmpEnvView env;
   unsigned int *bits;  /* ceil(n / 32) packed verdicts, bit set = VALID */
-  int stage;           /* 1: stage env in shared memory via cp.async.bulk */
+  int stage;           /* 1: stage env in shared memory via cp.async.bulk; 2: with the
+                          bound pairs behind the records (pair bound pass) */
   int pad_;
 } VmpValidateArgs;
 

@@ -101,11 +101,13 @@ __device__ __forceinline__ void vmp_fence_proxy_async() {
  * vmp_mbar_wait(bar, 0) before the first dereference when staged. */
 __device__ __forceinline__ const float4 *vmp_env_begin(const VmpEnvView &env, int stage,
                                                        float4 *smem,
-                                                       unsigned long long *bar) {
-  if (!stage || env.n_f4 == 0) return env.rec;
+                                                       unsigned long long *bar,
+                                                       bool with_pairs = false) {
+  const int n_f4 = with_pairs ? env.n_all_f4 : env.n_f4;
+  if (!stage || n_f4 == 0) return env.rec;
   if (threadIdx.x == 0) {
     vmp_mbar_init(bar, 1);
-    vmp_bulk_g2s(smem, env.rec, (unsigned)env.n_f4 * 16u, bar);
+    vmp_bulk_g2s(smem, env.rec, (unsigned)n_f4 * 16u, bar);
   }
   return smem;
 }
@@ -309,6 +311,25 @@ __device__ __forceinline__ vmp_f2 vmp_near2(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2
   w = vmp_fma2(x, vmp_bc(r0.x), w);
   w = vmp_fma2(y, vmp_bc(r0.y), w);
   w = vmp_fma2(z, vmp_bc(r0.z), w);
+  return w;
+}
+/* the same with the bound given as scalars (halves of a bound-pair record) */
+__device__ __forceinline__ vmp_f2 vmp_near2s(vmp_f2 x, vmp_f2 y, vmp_f2 z, vmp_f2 S, vmp_f2 m2rs,
+                                             float bx, float by, float bz, float bw, float r) {
+  vmp_f2 w = vmp_fma2(vmp_bc(r), m2rs, vmp_sub2(S, vmp_bc(bw)));
+  w = vmp_fma2(x, vmp_bc(bx), w);
+  w = vmp_fma2(y, vmp_bc(by), w);
+  w = vmp_fma2(z, vmp_bc(bz), w);
+  return w;
+}
+/* ONE group (scalar centre, S, -2R) against the TWO bounds of a pair record:
+ * the chain of vmp_near1 in both halves */
+__device__ __forceinline__ vmp_f2 vmp_near1x2(float x, float y, float z, float S, float m2rs,
+                                              vmp_f2 bx, vmp_f2 by, vmp_f2 bz, vmp_f2 bw, vmp_f2 r) {
+  vmp_f2 w = vmp_fma2(r, vmp_bc(m2rs), vmp_sub2(vmp_bc(S), bw));
+  w = vmp_fma2(vmp_bc(x), bx, w);
+  w = vmp_fma2(vmp_bc(y), by, w);
+  w = vmp_fma2(vmp_bc(z), bz, w);
   return w;
 }
 __device__ __forceinline__ float vmp_near1(float x, float y, float z, float S, float m2rs,
