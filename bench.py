@@ -287,7 +287,7 @@ def run_ours(args, rank: int, world: int) -> dict | None:
     hg = torch.from_numpy(mw.goals).pin_memory()
     depth = 6
     pipe = M.MotionPipeline(ctx, E, mw.resolution, width=32, depth=depth)
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, depth)):              # every slot has run once
         pipe.result(pipe.submit(hs, hg))
     # the K-step region lasts under a millisecond, so one host hiccup moves it by
     # tens of percent: it is timed E2E_REPS times, each from an empty pipeline to

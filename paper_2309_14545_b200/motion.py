@@ -151,6 +151,9 @@ class MotionValidator:
         return runtime.unpack_bits(self.host_bits(), self.n_edges)
 
 
+_NO_STEP_GRAPH = __import__("os").environ.get("VMP_EXP_NO_STEP_GRAPH") is not None   # experiments
+
+
 class MotionPipeline:
     """Multi-buffered stream of fixed-size edge batches from host memory.
 
@@ -165,7 +168,11 @@ class MotionPipeline:
     for that batch and returns its verdict words in pinned host memory; a
     slot is reused after ``depth`` submits, which first waits for the slot's
     previous batch.  Every batch still pays its own H2D and D2H transfers -
-    they are only overlapped with other batches' compute.
+    they are only overlapped with other batches' compute.  When the caller
+    refills the same pinned host buffers every step, the whole step - both
+    copies in, the three kernels, the copy out - is one CUDA graph per slot
+    (keyed by the source pointers): one launch per step instead of five API
+    calls (config 2: 35.3 -> 31.2 us per step end to end).
     """
 
     def __init__(self, ctx: ValidationContext, n_edges: int, resolution: float, *,
@@ -182,17 +189,46 @@ class MotionPipeline:
             st.wait_stream(origin)                              # buffers initialised
             ev.record(st)
         self.count = 0
+        # whole-step graphs (H2D copies + begin / rake / finalize + D2H copy) per
+        # slot, keyed by the pinned source buffers: a caller that refills the same
+        # pinned buffers every step pays one graph launch per step
+        self._step_graphs = [dict() for _ in self.slots]
+
+    def _step_graph(self, k: int, hs, hg):
+        """The slot's whole-step graph for these pinned source tensors, or None."""
+        if not (hs.is_pinned() and hg.is_pinned()) or self.slots[k].graph is None or _NO_STEP_GRAPH:
+            return None
+        key = (hs.data_ptr(), hg.data_ptr(), tuple(hs.shape), tuple(hg.shape))
+        cache = self._step_graphs[k]
+        if key not in cache:
+            if len(cache) >= 4:                                 # callers with ever-new buffers
+                return None
+            slot, st = self.slots[k], self.streams[k]
+            g = self.torch.cuda.CUDAGraph()
+            with self.torch.cuda.graph(g, stream=st):
+                slot.starts.copy_(hs, non_blocking=True)
+                slot.goals.copy_(hg, non_blocking=True)
+                slot._launch()
+                self.host[k].copy_(slot.bits, non_blocking=True)
+            cache[key] = (g, hs, hg)                            # keeps the buffers alive
+        return cache[key][0]
 
     def submit(self, starts, goals) -> int:
         k = self.count % len(self.slots)
         slot, st = self.slots[k], self.streams[k]
         if self.count >= len(self.slots):
             self.done[k].synchronize()                          # slot's previous batch is out
+        hs, hg = runtime._as_tensor(starts), runtime._as_tensor(goals)
+        whole = self._step_graph(k, hs, hg) if not hs.is_cuda and not hg.is_cuda else None
         with self.torch.cuda.stream(st):
-            slot.starts.copy_(runtime._as_tensor(starts), non_blocking=True)
-            slot.goals.copy_(runtime._as_tensor(goals), non_blocking=True)
-            slot()                                              # graph replay on the slot's stream
-            self.host[k].copy_(slot.bits, non_blocking=True)
+            if whole is not None:
+                slot.ctx.motion_checks += slot.n_edges
+                whole.replay()                                  # copies + kernels: one launch
+            else:
+                slot.starts.copy_(hs, non_blocking=True)
+                slot.goals.copy_(hg, non_blocking=True)
+                slot()                                          # graph replay on the slot's stream
+                self.host[k].copy_(slot.bits, non_blocking=True)
             self.done[k].record(st)
         self.count += 1
         return self.count - 1
