@@ -60,6 +60,19 @@ def test_motion_pipeline_overlapped_batches(cuda):
         for j, t in inflight:
             assert runtime.unpack_bits(pipe.result(t), E).tolist() == \
                 expect[j % len(batches)].tolist()
+    # the intended use: ONE pair of pinned buffers refilled in place every step
+    # (whole-step graphs keyed by the source pointers), then pageable numpy
+    # batches (no graph for the copies) through the same pipeline
+    pipe = M.MotionPipeline(ctx, E, mw.resolution, depth=2)
+    hs, hg = torch.empty_like(batches[0][0]).pin_memory(), torch.empty_like(batches[0][1]).pin_memory()
+    for j, (s, g) in enumerate(batches):
+        hs.copy_(s)
+        hg.copy_(g)
+        assert runtime.unpack_bits(pipe.result(pipe.submit(hs, hg)), E).tolist() == expect[j].tolist()
+    assert all(len(c) == 1 for c in pipe._step_graphs)
+    for j, (s, g) in enumerate(batches):
+        t = pipe.submit(s.numpy().copy(), g.numpy().copy())
+        assert runtime.unpack_bits(pipe.result(t), E).tolist() == expect[j].tolist()
 
 
 @pytest.mark.parametrize("early", [True, False])
