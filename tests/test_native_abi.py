@@ -68,3 +68,17 @@ def test_algorithmic_flops_matches_survey():
     rob = load_robot("arm7")
     f = codegen.algorithmic_flops(rob.program, rob.pairs, (32, 0, 0))
     assert f["fk"] == 151 and f["total"] == 3303
+
+
+def test_motion_workspace_sizing():
+    """Workspace = fixed part (header, queue words, 32,768 spare slots) + 136 bytes
+    per edge (failure record, n, 8 slots); batches above 2^22 edges run in
+    sub-batches on a 2^22-edge workspace (csrc/vmp.cu, csrc/vmp_abi.h)."""
+    L = _native.lib()
+    b = [int(L.vmp_motion_workspace_bytes(n)) for n in (0, 1, 4, 5, 4096, 1 << 22, 1 << 23)]
+    fixed = b[0]
+    assert fixed >= 16 * 32768 and fixed % 16 == 0
+    assert b[1] == b[2] == fixed + 4 * 136 and b[3] == fixed + 8 * 136      # padded to 4 edges
+    assert b[4] == fixed + 4096 * 136
+    assert b[5] == b[6] == fixed + (1 << 22) * 136
+    assert int(L.vmp_motion_workspace_bytes(-1)) == 0
