@@ -424,6 +424,27 @@ def test_motion_batch_sizes_agree(cuda, tiles):
             assert blk.cpu().numpy().tolist() == np.tile(ref[2].cpu().numpy(), tiles).tolist()
 
 
+def test_motion_sub_batches_above_4m_edges(cuda):
+    """Above 2^22 edges vmp_validate_motions runs sub-batches on one workspace
+    (csrc/vmp.cu): 1,025 copies of the config-2 edges give 1,025 copies of its
+    verdicts, n and block counts."""
+    torch = cuda
+    mw = workloads.config2()
+    rob = load_robot("arm7")
+    ctx = ValidationContext(rob.program, rob.model, rob.pairs, mw.env)
+    ref = M.validate_motions(ctx, mw.starts, mw.goals, mw.resolution, counts=True)
+    ref_v = runtime.unpack_bits(ref[0].cpu().numpy(), len(mw.starts))
+    tiles = 1025
+    s = torch.from_numpy(mw.starts).cuda().repeat(tiles, 1)
+    g = torch.from_numpy(mw.goals).cuda().repeat(tiles, 1)
+    assert len(s) > (1 << 22)
+    b, n, blk = M.validate_motions(ctx, s, g, mw.resolution, counts=True)
+    got = runtime.unpack_bits(b.cpu().numpy(), len(s)).reshape(tiles, -1)
+    assert (got == ref_v[None, :]).all()
+    assert (n.cpu().numpy().reshape(tiles, -1) == ref[1].cpu().numpy()[None, :]).all()
+    assert (blk.cpu().numpy().reshape(tiles, -1) == ref[2].cpu().numpy()[None, :]).all()
+
+
 def test_motion_very_long_edges_and_tiny_batches(cuda):
     """Very long edges (n up to ~57,000 states, ~1,800 chunks each) mixed with
     short ones, a zero-length edge, and batches of 0 / 1 edges - verdicts, n
